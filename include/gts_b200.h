@@ -1,0 +1,112 @@
+/*
+ * gts_b200.h -- C ABI of the B200 stencil backend (drop-in for the
+ * reference "gen" engine of stencilforge, arXiv 2311.08322 reproduction).
+ *
+ * Two kinds of shared objects implement this header:
+ *
+ *  1. libgts_b200.so (paper_2311_08322_b200/libgts_b200.so, built by
+ *     __graft_entry__.build()): device, memory, stream and event services,
+ *     the L2 flush used by the benchmark, and the halo pack/unpack kernels of
+ *     the horizontal domain decomposition.  Every gts_b200_* function below.
+ *
+ *  2. One generated module per compiled stencil
+ *     (<cache>/<fingerprint>/module.so), exporting GTS_B200_ENTRY below plus
+ *     the three gts_b200_module_* functions.
+ *
+ * All functions return 0 on success, otherwise a cudaError_t value or one of
+ * the GTS_B200_ERR_* codes; gts_b200_error_string() renders either.
+ * No torch or C++ types cross this boundary.
+ */
+#ifndef GTS_B200_H
+#define GTS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GTS_B200_ABI_VERSION 1
+
+#define GTS_B200_ERR_K_MIN 1001       /* nk below the stencil's k_min (runtime.py:178-183) */
+#define GTS_B200_ERR_ALLOC 1002       /* device arena allocation failed */
+#define GTS_B200_ERR_UNSUPPORTED 1003 /* domain exceeds 2^30 points per axis */
+
+/* ------------------------------------------------------------------------
+ * Generated per-stencil entry.
+ *
+ * Replaces the reference's generated C entry
+ *   void gts_run_<name>_<digest8>(int64 ni, nj, nk,
+ *        {T* base, int64 s_i, s_j, s_k, int64 o_i, o_j, o_k} per api field,
+ *        {double|float} per api scalar)
+ * (stencilforge backends/gen.py:5-14 and 269-284, pkg/README.md:142-156;
+ * bound by ctypes at gen.py:500-510) with:
+ *   - device pointers (element strides / origins unchanged: element (i,j,k)
+ *     is base[(i+o_i)*s_i + (j+o_j)*s_j + (k+o_k)*s_k]);
+ *   - every scalar passed as double (the debug/vec engines' semantics,
+ *     runtime.py:113; gen narrows f32 scalars, gen.py:276-277);
+ *   - a trailing cudaStream_t (as void*); the call is asynchronous on it;
+ *   - an int status instead of void.
+ * Symbol name: gts_run_<stencil name>_<first 8 hex digits of the
+ * fingerprint>, the gen mangling (gen.py:184-185).  Api pointers may alias.
+ * ---------------------------------------------------------------------- */
+typedef int (*gts_b200_entry_fn)(int64_t ni, int64_t nj, int64_t nk, ...);
+
+/* Exported by every generated module (one static CUDA runtime per module). */
+int gts_b200_module_set_device(int device);
+int gts_b200_module_abi(void);
+int gts_b200_module_release(void); /* frees the module's temporary arenas */
+
+/* ------------------------------------------------------------------------
+ * libgts_b200.so: runtime services.
+ * ---------------------------------------------------------------------- */
+int gts_b200_abi_version(void);
+const char* gts_b200_error_string(int status);
+
+int gts_b200_device_count(int* count);
+int gts_b200_set_device(int device);
+int gts_b200_get_device(int* device);
+/* SM count, L2 bytes, compute capability (major*10+minor), HBM bytes. */
+int gts_b200_device_info(int device, int* sm_count, int* l2_bytes, int* cc, size_t* hbm_bytes);
+
+/* Device memory for field storages (replaces the host numpy buffers of
+ * stencilforge storage.py:130-160 for device-resident fields). */
+int gts_b200_malloc(void** ptr, size_t bytes);
+int gts_b200_free(void* ptr);
+int gts_b200_host_alloc(void** ptr, size_t bytes); /* pinned host memory */
+int gts_b200_host_free(void* ptr);
+int gts_b200_memset(void* dst, int value, size_t bytes, void* stream);
+int gts_b200_memcpy_h2d(void* dst, const void* src, size_t bytes, void* stream);
+int gts_b200_memcpy_d2h(void* dst, const void* src, size_t bytes, void* stream);
+int gts_b200_memcpy_d2d(void* dst, const void* src, size_t bytes, void* stream);
+
+int gts_b200_stream_create(void** stream);
+int gts_b200_stream_destroy(void* stream);
+int gts_b200_stream_synchronize(void* stream);
+
+int gts_b200_event_create(void** event);
+int gts_b200_event_destroy(void* event);
+int gts_b200_event_record(void* event, void* stream);
+int gts_b200_event_synchronize(void* event);
+int gts_b200_event_elapsed_ms(float* ms, void* start, void* end);
+
+/* Evict L2 between timed iterations by writing a buffer of 2x the L2 size
+ * on the given stream (SURVEY.md 8(d) timing protocol). */
+int gts_b200_l2_flush(void* stream);
+
+/* Halo exchange support for the horizontal decomposition:
+ * copy the box [i0,i0+ni) x [j0,j0+nj) x [k0,k0+nk) (storage coordinates,
+ * element strides s_i/s_j/s_k, itemsize 4 or 8) of a strided field to / from
+ * a contiguous buffer laid out (k, i, j) with j fastest. */
+int gts_b200_pack_box(void* buf, const void* base, int64_t s_i, int64_t s_j, int64_t s_k,
+                      int64_t i0, int64_t j0, int64_t k0, int64_t ni, int64_t nj, int64_t nk,
+                      int itemsize, void* stream);
+int gts_b200_unpack_box(void* base, const void* buf, int64_t s_i, int64_t s_j, int64_t s_k,
+                        int64_t i0, int64_t j0, int64_t k0, int64_t ni, int64_t nj, int64_t nk,
+                        int itemsize, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GTS_B200_H */

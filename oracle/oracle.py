@@ -1,0 +1,218 @@
+"""CPU parity checker for the hdiff / vadv hot path -- TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s cpu_baseline /
+``--impl reference`` legs may import this module.  The product package
+(``paper_2311_08322_b200``) never imports, links or executes anything under
+``oracle/``.
+
+Two independent restatements of the reference algorithms live here:
+
+* ``libgts_oracle.so`` (``gts_oracle.c``): plain C with the reference gen
+  engine's flags (``-O3 -fopenmp -ffp-contract=off``, stencilforge
+  ``backends/gen.py:64-67``) and the gen entry ABI (``gen.py:5-14``).  It is
+  the large-size oracle and the CPU baseline.
+* ``hdiff_np`` / ``vadv_np``: NumPy restatements of ``kernels/hdiff.gts:3-15``
+  and ``kernels/vadv.gts:4-16`` in the association order of the lowered IR
+  (``pkg/tests/golden/hdiff_implementation.txt:11-24``).
+
+Pinning: ``tests/test_oracle.py`` checks both restatements bitwise against
+the golden vectors in ``tests/golden/`` that ``tests/golden/make_golden.py``
+produced by running the reference's own ``vec`` and ``debug`` backends.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from pathlib import Path
+from typing import Optional
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+LIB_PATH = HERE / "libgts_oracle.so"
+
+_lib: Optional[ctypes.CDLL] = None
+
+
+def build(force: bool = False) -> Path:
+    """Compile libgts_oracle.so with the committed Makefile."""
+    if force or not LIB_PATH.exists() or (
+        LIB_PATH.stat().st_mtime < (HERE / "gts_oracle.c").stat().st_mtime
+    ):
+        env = dict(os.environ)
+        env.pop("CC", None)
+        subprocess.run(["make", "-C", str(HERE), "-B" if force else "all"],
+                       check=True, capture_output=True, env=env)
+    return LIB_PATH
+
+
+def load() -> ctypes.CDLL:
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            build()
+        lib = ctypes.CDLL(str(LIB_PATH))
+        i64 = ctypes.c_int64
+        field = [ctypes.c_void_p] + [i64] * 6
+        for name in ("oracle_hdiff_f64", "oracle_hdiff_f32"):
+            fn = getattr(lib, name)
+            fn.argtypes = [i64] * 3 + field * 2 + [ctypes.c_double, ctypes.c_int]
+            fn.restype = ctypes.c_int
+        for name in ("oracle_vadv_f64", "oracle_vadv_f32"):
+            fn = getattr(lib, name)
+            fn.argtypes = [i64] * 3 + field * 5 + [ctypes.c_int]
+            fn.restype = ctypes.c_int
+        lib.oracle_max_threads.restype = ctypes.c_int
+        _lib = lib
+    return _lib
+
+
+def max_threads() -> int:
+    return int(load().oracle_max_threads())
+
+
+def _sfx(dtype) -> str:
+    return "f32" if np.dtype(dtype) == np.float32 else "f64"
+
+
+def _field_args(arr: np.ndarray, origin) -> list:
+    """(base, strides in elements, origin) of a logical (i,j,k) array view."""
+    item = arr.dtype.itemsize
+    strides = [s // item for s in arr.strides]
+    return [arr.ctypes.data, *strides, *origin]
+
+
+# ---------------------------------------------------------------------------
+# C oracle on logical arrays
+# ---------------------------------------------------------------------------
+
+
+def hdiff_c(inp: np.ndarray, coeff: float, nthreads: int = 0) -> np.ndarray:
+    """hdiff on a (ni+4, nj+4, nk) logical block; returns (ni, nj, nk)."""
+    inp = np.ascontiguousarray(inp)
+    ni, nj, nk = inp.shape[0] - 4, inp.shape[1] - 4, inp.shape[2]
+    out = np.zeros((ni, nj, nk), dtype=inp.dtype)
+    fn = getattr(load(), f"oracle_hdiff_{_sfx(inp.dtype)}")
+    rc = fn(ni, nj, nk, *_field_args(inp, (2, 2, 0)), *_field_args(out, (0, 0, 0)),
+            float(coeff), int(nthreads))
+    if rc:
+        raise RuntimeError(f"oracle_hdiff failed: {rc}")
+    return out
+
+
+def vadv_c(a, b, c, d, nthreads: int = 0) -> np.ndarray:
+    arrs = [np.ascontiguousarray(v) for v in (a, b, c, d)]
+    x = np.zeros_like(arrs[0])
+    ni, nj, nk = x.shape
+    fn = getattr(load(), f"oracle_vadv_{_sfx(x.dtype)}")
+    args = []
+    for v in arrs + [x]:
+        args += _field_args(v, (0, 0, 0))
+    rc = fn(ni, nj, nk, *args, int(nthreads))
+    if rc:
+        raise RuntimeError(f"oracle_vadv failed: {rc}")
+    return x
+
+
+def run_on_storages(kernel: str, dtype: str, domain, fields: dict, scalars: dict,
+                    nthreads: int = 0) -> None:
+    """Run the C oracle directly on FieldStorage-like objects (anything with
+    ``base_address()``, ``strides`` and ``origin``), gen-ABI style.  Used by
+    bench.py's CPU baseline on the same storages the GPU path consumes."""
+    lib = load()
+    args: list = [int(domain[0]), int(domain[1]), int(domain[2])]
+    names = ("inp", "out") if kernel == "hdiff" else ("a", "b", "c", "d", "x")
+    for n in names:
+        st = fields[n]
+        args += [st.base_address(), *st.strides, *st.origin]
+    if kernel == "hdiff":
+        args.append(float(scalars["coeff"]))
+    args.append(int(nthreads))
+    rc = getattr(lib, f"oracle_{kernel}_{dtype}")(*args)
+    if rc:
+        raise RuntimeError(f"oracle_{kernel} failed: {rc}")
+
+
+# ---------------------------------------------------------------------------
+# NumPy restatements (second, independent route)
+# ---------------------------------------------------------------------------
+
+
+def hdiff_np(inp: np.ndarray, coeff: float) -> np.ndarray:
+    """NumPy hdiff with the reference's stage order and f32 narrowing of the
+    temporaries when the input is f32 (analysis.py:424-443)."""
+    tdt = inp.dtype
+    x = inp.astype(np.float64)
+    ni, nj = inp.shape[0] - 4, inp.shape[1] - 4
+
+    def I(di, dj, a=x, lo=2, ei=(0, 0), ej=(0, 0)):
+        return a[lo + ei[0] + di: lo + ni + ei[1] + di, lo + ej[0] + dj: lo + nj + ej[1] + dj]
+
+    # lap over [-1, ni+1) x [-1, nj+1)
+    e = ((-1, 1), (-1, 1))
+    lap = (4.0 * I(0, 0, ei=e[0], ej=e[1])) - (
+        ((I(-1, 0, ei=e[0], ej=e[1]) + I(1, 0, ei=e[0], ej=e[1])) + I(0, -1, ei=e[0], ej=e[1]))
+        + I(0, 1, ei=e[0], ej=e[1]))
+    lap = lap.astype(tdt).astype(np.float64)  # temp store narrowing (no-op for f64)
+
+    def L(di, dj, ei, ej):  # lap origin is (1, 1)
+        return lap[1 + ei[0] + di: 1 + ni + ei[1] + di, 1 + ej[0] + dj: 1 + nj + ej[1] + dj]
+
+    ex, ey = ((-1, 0), (0, 0)), ((0, 0), (-1, 0))
+    dfx = L(1, 0, *ex) - L(0, 0, *ex)
+    flx = np.where((dfx * (I(1, 0, ei=ex[0], ej=ex[1]) - I(0, 0, ei=ex[0], ej=ex[1]))) > 0.0,
+                   0.0, dfx).astype(tdt).astype(np.float64)
+    dfy = L(0, 1, *ey) - L(0, 0, *ey)
+    fly = np.where((dfy * (I(0, 1, ei=ey[0], ej=ey[1]) - I(0, 0, ei=ey[0], ej=ey[1]))) > 0.0,
+                   0.0, dfy).astype(tdt).astype(np.float64)
+    # flx origin (1, 0); fly origin (0, 1)
+    out = I(0, 0) - (coeff * (((flx[1:, :] - flx[:-1, :]) + fly[:, 1:]) - fly[:, :-1]))
+    return out.astype(tdt)
+
+
+def vadv_np(a, b, c, d) -> np.ndarray:
+    """NumPy Thomas sweep, level by level over whole planes like the
+    reference's vec engine (vec.py:160-166)."""
+    tdt = np.result_type(a.dtype, b.dtype, c.dtype, d.dtype)
+    tdt = np.float32 if tdt == np.float32 else np.float64
+    A, B, C, D = (v.astype(np.float64) for v in (a, b, c, d))
+    nk = a.shape[2]
+    cp = np.empty(a.shape, dtype=tdt)
+    dp = np.empty(a.shape, dtype=tdt)
+    cp[:, :, 0] = C[:, :, 0] / B[:, :, 0]
+    dp[:, :, 0] = D[:, :, 0] / B[:, :, 0]
+    for k in range(1, nk):
+        cpm = cp[:, :, k - 1].astype(np.float64)
+        cp[:, :, k] = C[:, :, k] / (B[:, :, k] - (A[:, :, k] * cpm))
+        dp[:, :, k] = (D[:, :, k] - (A[:, :, k] * dp[:, :, k - 1].astype(np.float64))) / (
+            B[:, :, k] - (A[:, :, k] * cpm))
+    x = np.empty(a.shape, dtype=a.dtype)
+    x[:, :, nk - 1] = dp[:, :, nk - 1]
+    for k in range(nk - 2, -1, -1):
+        x[:, :, k] = dp[:, :, k].astype(np.float64) - (
+            cp[:, :, k].astype(np.float64) * x[:, :, k + 1].astype(np.float64))
+    return x
+
+
+def max_rel(a: np.ndarray, b: np.ndarray) -> float:
+    """The reference's cross-backend metric (test_acceptance.py:50-54,
+    cli.py:295-296)."""
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    if a.size == 0:
+        return 0.0
+    denom = np.maximum(np.maximum(np.abs(a), np.abs(b)), 1e-30)
+    return float(np.max(np.abs(a - b) / denom))
+
+
+def make_diagonally_dominant(rng: np.random.Generator, shape):
+    """Restatement of the reference's vadv input generator
+    (oracles.py:81-89): a, c ~ U(0.1, 1), b = |a| + |c| + U(0.5, 1.5),
+    d ~ U(-1, 1), drawn in that order from one generator."""
+    a = rng.uniform(0.1, 1.0, shape)
+    c = rng.uniform(0.1, 1.0, shape)
+    b = np.abs(a) + np.abs(c) + rng.uniform(0.5, 1.5, shape)
+    d = rng.uniform(-1.0, 1.0, shape)
+    return a, b, c, d

@@ -1,0 +1,437 @@
+"""Code generation: lowering ``Plan`` -> one CUDA translation unit per stencil.
+
+The TU instantiates the hand-written templates in ``csrc/templates/`` with
+stage bodies emitted from the reference IR, and exports the drop-in entry
+
+    int gts_run_<name>_<digest8>(int64 ni, int64 nj, int64 nk,
+                                 {T* base, int64 s_i, s_j, s_k, o_i, o_j, o_k}
+                                     per api field in declaration order,
+                                 double per api scalar in declaration order,
+                                 void* stream)
+
+i.e. the reference gen entry ABI (stencilforge ``backends/gen.py:5-14,
+269-284``, ``pkg/README.md:142-156``) with device pointers, a trailing CUDA
+stream and an ``int`` status (0 = ok, else a cudaError_t or a GTS_ERR_* code).
+Scalars are always passed as double, following the debug/vec engines
+(``runtime.py:113``) rather than gen's float narrowing of f32 scalars.
+
+Numerics contract: f64 arithmetic in the IR's association
+order, f32 operands widened on read and narrowed on every store (register
+temporaries included), NaN-propagating min/max (``gen.py:257-266``), IEEE
+division (nvcc default ``-prec-div=true``), no FMA contraction
+(``--fmad=false``, mirroring gen's ``-ffp-contract=off``, ``gen.py:64-67``),
+exact hex literals (``gen.py:111-116``).
+"""
+
+from __future__ import annotations
+
+import math
+from typing import Optional
+
+from ._host import ir
+from .lowering import Plan, always_writes, reads, writes
+
+GTS_ERR_K_MIN = 1001
+GTS_ERR_ALLOC = 1002
+GTS_ERR_UNSUPPORTED = 1003
+
+_BUILTIN_CUDA = {
+    "abs": "fabs",
+    "min": "gts_min",
+    "max": "gts_max",
+    "sqrt": "sqrt",
+    "exp": "exp",
+    "log": "log",
+    "pow": "pow",
+    "floor": "floor",
+    "ceil": "ceil",
+}
+_BINOP = {"and": "&&", "or": "||"}
+
+
+def c_float(value: float) -> str:
+    if math.isnan(value):
+        return "GTS_NAN"
+    if math.isinf(value):
+        return "(-GTS_INF)" if value < 0 else "GTS_INF"
+    return float(value).hex()
+
+
+def entry_name(impl, fp) -> str:
+    """Same mangling as the reference gen engine (gen.py:184-185)."""
+    return f"gts_run_{impl.name}_{fp.short}"
+
+
+class _Ctx:
+    """How a field access at an offset is spelled inside one kernel."""
+
+    def __init__(self, dtypes: dict):
+        self.dtypes = dtypes  # name -> "f32" | "f64"
+
+    def read(self, name: str, off) -> str:
+        raise NotImplementedError
+
+
+class _MemCtx(_Ctx):
+    """Every access goes to device memory at (i, j, k) + offset."""
+
+    def __init__(self, dtypes: dict, kvar: str = "k"):
+        super().__init__(dtypes)
+        self.kvar = kvar
+
+    def addr(self, name: str, off) -> str:
+        di, dj, dk = off
+        ii = f"(i{di:+d})" if di else "i"
+        jj = f"(j{dj:+d})" if dj else "j"
+        kk = f"({self.kvar}{dk:+d})" if dk else self.kvar
+        return f"GTS_AT(p.f_{name}, {ii}, {jj}, {kk})"
+
+    def read(self, name: str, off) -> str:
+        return f"((double){self.addr(name, off)})"
+
+
+def emit_expr(e, ctx: _Ctx) -> str:
+    if isinstance(e, ir.Literal):
+        return c_float(float(e.value))
+    if isinstance(e, ir.ScalarRef):
+        return f"p.sc_{e.name}"
+    if isinstance(e, ir.FieldAccess):
+        return ctx.read(e.field, e.offset)
+    if isinstance(e, ir.UnaryOp):
+        inner = emit_expr(e.operand, ctx)
+        return f"(!{inner})" if e.op == "not" else f"(-{inner})"
+    if isinstance(e, ir.BinaryOp):
+        op = _BINOP.get(e.op, e.op)
+        return f"({emit_expr(e.left, ctx)} {op} {emit_expr(e.right, ctx)})"
+    if isinstance(e, ir.BuiltinCall):
+        args = ", ".join(emit_expr(a, ctx) for a in e.args)
+        return f"{_BUILTIN_CUDA[e.name]}({args})"
+    raise TypeError(f"cannot generate code for {type(e).__name__}")
+
+
+# ---------------------------------------------------------------------------
+# Statement emission for memory-backed kernels (pstage / plane / column)
+# ---------------------------------------------------------------------------
+
+
+def _store_mem(name: str, value: str, ctx: _MemCtx, ctype: dict) -> str:
+    return f"{ctx.addr(name, (0, 0, 0))} = ({ctype[name]})({value});"
+
+
+def emit_stmt_mem(stmt, ctx: _MemCtx, ctype: dict, indent: str, out: list,
+                  on_write=None) -> None:
+    if isinstance(stmt, ir.Assign):
+        name = stmt.target.field
+        out.append(f"{indent}{{ const double v_ = {emit_expr(stmt.value, ctx)};")
+        out.append(f"{indent}  {_store_mem(name, 'v_', ctx, ctype)}")
+        if on_write is not None:
+            extra = on_write(name, "v_")
+            if extra:
+                out.append(f"{indent}  {extra}")
+        out.append(f"{indent}}}")
+        return
+    if isinstance(stmt, ir.If):
+        out.append(f"{indent}if ({emit_expr(stmt.cond, ctx)}) {{")
+        for s in stmt.then_body:
+            emit_stmt_mem(s, ctx, ctype, indent + "  ", out, on_write)
+        if stmt.else_body:
+            out.append(f"{indent}}} else {{")
+            for s in stmt.else_body:
+                emit_stmt_mem(s, ctx, ctype, indent + "  ", out, on_write)
+        out.append(f"{indent}}}")
+        return
+    raise TypeError(f"cannot generate code for {type(stmt).__name__}")
+
+
+# ---------------------------------------------------------------------------
+# Column kernel (k-caches)
+# ---------------------------------------------------------------------------
+
+
+class _ColumnCtx(_MemCtx):
+    """Memory accesses, except fields with an active k-cache: reads at the
+    current level use ``cur_<f>``; reads ``s`` levels behind in iteration
+    order use ``prev<s>_<f>``."""
+
+    def __init__(self, dtypes, direction: int, cached: dict):
+        super().__init__(dtypes)
+        self.direction = direction  # +1 FORWARD/PARALLEL, -1 BACKWARD
+        self.cached = cached  # name -> depth (levels behind kept)
+
+    def read(self, name, off):
+        if name in self.cached and not (off[0] or off[1]):
+            s = -off[2] * self.direction
+            if off[2] == 0:
+                return f"cur_{name}"
+            if 1 <= s <= self.cached[name]:
+                return f"prev{s}_{name}"
+        return super().read(name, off)
+
+
+def _bound(b) -> str:
+    return f"{b.offset}" if b.ref == ir.START else f"(nk + {b.offset})"
+
+
+def _column_kernel(kname: str, plan: Plan, kplan, ctype: dict, dtypes: dict) -> list:
+    impl = plan.impl
+    out: list = []
+    w = out.append
+    w(f"__global__ void __launch_bounds__(GTS_COL_THREADS) {kname}(const __grid_constant__ GtsParams p) {{")
+    w("  const int j = blockIdx.x * GTS_COL_TJ + (threadIdx.x % GTS_COL_TJ);")
+    w("  const int i = blockIdx.y * (GTS_COL_THREADS / GTS_COL_TJ) + (threadIdx.x / GTS_COL_TJ);")
+    w("  if (i >= p.ni || j >= p.nj) return;")
+    w("  const int nk = p.nk;")
+    for m in kplan.multistages:
+        ms = impl.multistages[m]
+        direction = -1 if ms.order == ir.BACKWARD else 1
+        ms_writes = set()
+        for st in ms.stages:
+            ms_writes |= writes(st.body)
+        # k-cache depth per written field read behind the sweep
+        cached: dict = {}
+        if ms.order != ir.PARALLEL:
+            for st in ms.stages:
+                for acc in reads(st.body):
+                    if acc.field in ms_writes and not (acc.offset[0] or acc.offset[1]) and acc.offset[2]:
+                        s = -acc.offset[2] * direction
+                        if s > 0:
+                            cached[acc.field] = max(cached.get(acc.field, 0), s)
+        w(f"  {{ // multistage {m}: {ms.order}")
+        for f, depth in sorted(cached.items()):
+            for s in range(1, depth + 1):
+                w(f"    double prev{s}_{f} = GTS_NAN;")
+        ctx = _ColumnCtx(dtypes, direction, cached)
+        for interval, stages in _interval_groups(ms):
+            w("    {")
+            w(f"      const int k0 = {_bound(interval.start)}, k1 = {_bound(interval.end)};")
+            w("      if (k0 < k1) {")
+            # initialise the k-cache from memory for the levels behind the first
+            group_reads_behind: dict = {}
+            for st in stages:
+                for acc in reads(st.body):
+                    if acc.field in cached and not (acc.offset[0] or acc.offset[1]):
+                        s = -acc.offset[2] * direction
+                        if s > 0:
+                            group_reads_behind[acc.field] = max(group_reads_behind.get(acc.field, 0), s)
+            kfirst = "k0" if direction > 0 else "(k1 - 1)"
+            for f, depth in sorted(group_reads_behind.items()):
+                for s in range(1, depth + 1):
+                    kk = f"({kfirst} - {s})" if direction > 0 else f"({kfirst} + {s})"
+                    w(f"        prev{s}_{f} = ((double)GTS_AT(p.f_{f}, i, j, {kk}));")
+            if direction > 0:
+                w("        for (int k = k0; k < k1; ++k) {")
+            else:
+                w("        for (int k = k1 - 1; k >= k0; --k) {")
+            # current-level registers for cached fields
+            for f in sorted(cached):
+                need_load = True
+                for st in stages:
+                    touched_read = any(acc.field == f and acc.offset == (0, 0, 0) for acc in reads(st.body))
+                    if touched_read:
+                        break
+                    if f in always_writes(st.body) and isinstance(st.body, ir.Assign):
+                        need_load = False
+                        break
+                    if f in writes(st.body):
+                        break
+                if need_load:
+                    w(f"          double cur_{f} = ((double)GTS_AT(p.f_{f}, i, j, k));")
+                else:
+                    w(f"          double cur_{f};")
+
+            def on_write(name, v):
+                if name in cached:
+                    return f"cur_{name} = (double)({ctype[name]})({v});"
+                return ""
+
+            for st in stages:
+                emit_stmt_mem(st.body, ctx, ctype, "          ", out, on_write)
+            for f, depth in sorted(cached.items()):
+                for s in range(depth, 1, -1):
+                    w(f"          prev{s}_{f} = prev{s - 1}_{f};")
+                w(f"          prev1_{f} = cur_{f};")
+            w("        }")
+            w("      }")
+            w("    }")
+        w("  }")
+    w("}")
+    return out
+
+
+def _interval_groups(ms) -> list:
+    """backends/common.py:38-46."""
+    groups: list = []
+    for stage in ms.stages:
+        if groups and groups[-1][0] == stage.interval:
+            groups[-1][1].append(stage)
+        else:
+            groups.append((stage.interval, [stage]))
+    return groups
+
+
+# ---------------------------------------------------------------------------
+# Point kernels (pstage / plane)
+# ---------------------------------------------------------------------------
+
+
+def _point_kernel(kname: str, stage, ctype: dict, dtypes: dict) -> list:
+    out: list = []
+    w = out.append
+    w(f"__global__ void __launch_bounds__(256) {kname}(const __grid_constant__ GtsParams p, "
+      "int i0, int i1, int j0, int j1, int kbase) {")
+    w("  const int j = j0 + blockIdx.x * 32 + (threadIdx.x & 31);")
+    w("  const int i = i0 + blockIdx.y * 8 + (threadIdx.x >> 5);")
+    w("  const int k = kbase + blockIdx.z;")
+    w("  if (i >= i1 || j >= j1) return;")
+    emit_stmt_mem(stage.body, _MemCtx(dtypes), ctype, "  ", out)
+    w("}")
+    return out
+
+
+# ---------------------------------------------------------------------------
+# Translation unit
+# ---------------------------------------------------------------------------
+
+
+def generate_source(plan: Plan, fp, options: Optional[dict] = None) -> str:
+    impl = plan.impl
+    from . import codegen_parallel  # fused PARALLEL template instantiation
+
+    ct = {ir.F32: "float", ir.F64: "double"}
+    dtypes = {f.name: f.dtype for f in impl.api_fields}
+    dtypes.update({t.name: t.dtype for t in impl.temporaries})
+    ctype = {n: ct[d] for n, d in dtypes.items()}
+    temps = {t.name: t for t in impl.temporaries}
+
+    out: list = []
+    w = out.append
+    w("// generated by paper_2311_08322_b200; do not edit")
+    w(f"// stencil: {impl.name}  fingerprint: {fp.digest}")
+    w(f"// plan: {' '.join(plan.describe())}")
+    w('#include "gts_common.cuh"')
+    if any(k.kind == "pfused" for k in plan.kernels):
+        w('#include "gts_parallel.cuh"')
+    w("")
+    w("struct GtsParams {")
+    w("  int ni, nj, nk;")
+    for f in impl.api_fields:
+        w(f"  GtsField<{ctype[f.name]}> f_{f.name};")
+    for t in plan.global_temps:
+        w(f"  GtsField<{ctype[t]}> f_{t};")
+    for s in impl.api_scalars:
+        w(f"  double sc_{s.name};")
+    w("};")
+    w("")
+
+    launches: list = []  # host-side launch code lines
+    for kidx, k in enumerate(plan.kernels):
+        kname = f"gts_k{kidx}_{k.kind}"
+        if k.kind == "pstage":
+            st = k.stages[0].stage
+            out.extend(_point_kernel(kname, st, ctype, dtypes))
+            e = st.compute_extent
+            launches += [
+                "  {",
+                f"    const int k0 = {_bound(st.interval.start)}, k1 = {_bound(st.interval.end)};",
+                f"    const int i0 = {e.lo[0]}, i1 = (int)ni + {e.hi[0]};",
+                f"    const int j0 = {e.lo[1]}, j1 = (int)nj + {e.hi[1]};",
+                "    if (k0 < k1 && i0 < i1 && j0 < j1) {",
+                "      for (int kb = k0; kb < k1; kb += 65535) {",
+                "        dim3 grid((unsigned)((j1 - j0 + 31) / 32), (unsigned)((i1 - i0 + 7) / 8),"
+                " (unsigned)((k1 - kb) < 65535 ? (k1 - kb) : 65535));",
+                f"        {kname}<<<grid, 256, 0, st>>>(p, i0, i1, j0, j1, kb);",
+                "      }",
+                "    }",
+                "  }",
+            ]
+        elif k.kind == "plane":
+            ms = impl.multistages[k.multistages[0]]
+            stage_names = {}
+            for r in k.stages:
+                nm = f"{kname}_s{r.idx}"
+                stage_names[id(r.stage)] = nm
+                out.extend(_point_kernel(nm, r.stage, ctype, dtypes))
+            launches.append("  {")
+            for interval, stages in _interval_groups(ms):
+                launches.append(f"    {{ const int k0 = {_bound(interval.start)}, k1 = {_bound(interval.end)};")
+                if ms.order == ir.BACKWARD:
+                    launches.append("      for (int k = k1 - 1; k >= k0; --k) {")
+                else:
+                    launches.append("      for (int k = k0; k < k1; ++k) {")
+                for st in stages:
+                    e = st.compute_extent
+                    launches += [
+                        f"        {{ const int i0 = {e.lo[0]}, i1 = (int)ni + {e.hi[0]};",
+                        f"          const int j0 = {e.lo[1]}, j1 = (int)nj + {e.hi[1]};",
+                        "          if (i0 < i1 && j0 < j1) {",
+                        "            dim3 grid((unsigned)((j1 - j0 + 31) / 32), (unsigned)((i1 - i0 + 7) / 8), 1);",
+                        f"            {stage_names[id(st)]}<<<grid, 256, 0, st>>>(p, i0, i1, j0, j1, k);",
+                        "          }",
+                        "        }",
+                    ]
+                launches.append("      }")
+                launches.append("    }")
+            launches.append("  }")
+        elif k.kind == "column":
+            out.extend(_column_kernel(kname, plan, k, ctype, dtypes))
+            launches += [
+                "  {",
+                "    dim3 grid((unsigned)((nj + GTS_COL_TJ - 1) / GTS_COL_TJ),"
+                " (unsigned)((ni + (GTS_COL_THREADS / GTS_COL_TJ) - 1) / (GTS_COL_THREADS / GTS_COL_TJ)), 1);",
+                f"    {kname}<<<grid, GTS_COL_THREADS, 0, st>>>(p);",
+                "  }",
+            ]
+        elif k.kind == "pfused":
+            code, launch = codegen_parallel.emit(kname, plan, k, ctype, dtypes)
+            out.extend(code)
+            launches += launch
+        else:
+            raise ValueError(k.kind)
+        w("")
+
+    # ---- host entry ----
+    params = ["int64_t ni", "int64_t nj", "int64_t nk"]
+    for f in impl.api_fields:
+        params.append(f"{ctype[f.name]}* f_{f.name}")
+        params += [f"int64_t s_{f.name}_{a}" for a in "ijk"]
+        params += [f"int64_t o_{f.name}_{a}" for a in "ijk"]
+    for s in impl.api_scalars:
+        params.append(f"double sc_{s.name}")
+    params.append("void* stream")
+    name = entry_name(impl, fp)
+    w('extern "C" __attribute__((visibility("default")))')
+    w(f"int {name}(" + ", ".join(params) + ") {")
+    w("  if (ni <= 0 || nj <= 0 || nk <= 0) return 0;")
+    w(f"  if (nk < {impl.k_min}) return {GTS_ERR_K_MIN};")
+    w("  if (ni > 0x3fffffff || nj > 0x3fffffff || nk > 0x3fffffff) return %d;" % GTS_ERR_UNSUPPORTED)
+    w("  cudaStream_t st = (cudaStream_t)stream;")
+    w("  GtsParams p;")
+    w("  p.ni = (int)ni; p.nj = (int)nj; p.nk = (int)nk;")
+    for f in impl.api_fields:
+        n = f.name
+        w(f"  p.f_{n} = gts_field(f_{n}, s_{n}_i, s_{n}_j, s_{n}_k, o_{n}_i, o_{n}_j, o_{n}_k);")
+    for s in impl.api_scalars:
+        w(f"  p.sc_{s.name} = sc_{s.name};")
+    if plan.global_temps:
+        w("  // device arena for temporaries: shape = domain + extent (common.py:58-69),")
+        w("  // k outermost, j contiguous, rows padded to 128 B; persistent across calls")
+        w("  size_t arena_bytes = 0;")
+        for t in plan.global_temps:
+            e = temps[t].extent
+            w(f"  const int64_t td_{t}_i = ni + {e.hi[0] - e.lo[0]}, td_{t}_j = nj + {e.hi[1] - e.lo[1]};")
+            w(f"  const int64_t tp_{t} = gts_pad_row(td_{t}_j, sizeof({ctype[t]}));")
+            w(f"  const size_t toff_{t} = arena_bytes;")
+            w(f"  arena_bytes += gts_round_up((size_t)(td_{t}_i * tp_{t} * nk) * sizeof({ctype[t]}), 256);")
+        w("  char* arena = (char*)gts_arena(arena_bytes, st);")
+        w(f"  if (!arena) return {GTS_ERR_ALLOC};")
+        for t in plan.global_temps:
+            e = temps[t].extent
+            w(f"  p.f_{t} = gts_field(({ctype[t]}*)(arena + toff_{t}), tp_{t}, 1, td_{t}_i * tp_{t},"
+              f" {-e.lo[0]}, {-e.lo[1]}, 0);")
+        for t in plan.nan_fill_temps:
+            w(f"  gts_fill_nan(arena + toff_{t}, (size_t)(td_{t}_i * tp_{t} * nk), sizeof({ctype[t]}), st);")
+    out.extend(launches)
+    w("  return (int)cudaGetLastError();")
+    w("}")
+    w("")
+    return "\n".join(out)

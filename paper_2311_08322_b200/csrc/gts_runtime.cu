@@ -1,0 +1,183 @@
+// gts_runtime.cu -- libgts_b200.so: runtime services of the B200 stencil
+// backend (declared in include/gts_b200.h).
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include <mutex>
+
+#include "gts_b200.h"
+
+#define GTS_EXPORT extern "C" __attribute__((visibility("default")))
+
+GTS_EXPORT int gts_b200_abi_version(void) { return GTS_B200_ABI_VERSION; }
+
+GTS_EXPORT const char* gts_b200_error_string(int status) {
+  switch (status) {
+    case 0:
+      return "success";
+    case GTS_B200_ERR_K_MIN:
+      return "vertical domain below the stencil's k_min";
+    case GTS_B200_ERR_ALLOC:
+      return "device arena allocation failed";
+    case GTS_B200_ERR_UNSUPPORTED:
+      return "domain too large (more than 2^30 points along an axis)";
+    default:
+      return cudaGetErrorString((cudaError_t)status);
+  }
+}
+
+GTS_EXPORT int gts_b200_device_count(int* count) { return (int)cudaGetDeviceCount(count); }
+GTS_EXPORT int gts_b200_set_device(int device) { return (int)cudaSetDevice(device); }
+GTS_EXPORT int gts_b200_get_device(int* device) { return (int)cudaGetDevice(device); }
+
+GTS_EXPORT int gts_b200_device_info(int device, int* sm_count, int* l2_bytes, int* cc,
+                                    size_t* hbm_bytes) {
+  cudaDeviceProp prop;
+  cudaError_t e = cudaGetDeviceProperties(&prop, device);
+  if (e != cudaSuccess) return (int)e;
+  if (sm_count) *sm_count = prop.multiProcessorCount;
+  if (l2_bytes) *l2_bytes = prop.l2CacheSize;
+  if (cc) *cc = prop.major * 10 + prop.minor;
+  if (hbm_bytes) *hbm_bytes = prop.totalGlobalMem;
+  return 0;
+}
+
+GTS_EXPORT int gts_b200_malloc(void** ptr, size_t bytes) {
+  return (int)cudaMalloc(ptr, bytes ? bytes : 1);
+}
+GTS_EXPORT int gts_b200_free(void* ptr) { return (int)cudaFree(ptr); }
+GTS_EXPORT int gts_b200_host_alloc(void** ptr, size_t bytes) {
+  return (int)cudaHostAlloc(ptr, bytes ? bytes : 1, cudaHostAllocPortable);
+}
+GTS_EXPORT int gts_b200_host_free(void* ptr) { return (int)cudaFreeHost(ptr); }
+
+GTS_EXPORT int gts_b200_memset(void* dst, int value, size_t bytes, void* stream) {
+  return (int)cudaMemsetAsync(dst, value, bytes, (cudaStream_t)stream);
+}
+GTS_EXPORT int gts_b200_memcpy_h2d(void* dst, const void* src, size_t bytes, void* stream) {
+  return (int)cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, (cudaStream_t)stream);
+}
+GTS_EXPORT int gts_b200_memcpy_d2h(void* dst, const void* src, size_t bytes, void* stream) {
+  return (int)cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, (cudaStream_t)stream);
+}
+GTS_EXPORT int gts_b200_memcpy_d2d(void* dst, const void* src, size_t bytes, void* stream) {
+  return (int)cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, (cudaStream_t)stream);
+}
+
+GTS_EXPORT int gts_b200_stream_create(void** stream) {
+  return (int)cudaStreamCreateWithFlags((cudaStream_t*)stream, cudaStreamNonBlocking);
+}
+GTS_EXPORT int gts_b200_stream_destroy(void* stream) {
+  return (int)cudaStreamDestroy((cudaStream_t)stream);
+}
+GTS_EXPORT int gts_b200_stream_synchronize(void* stream) {
+  return (int)cudaStreamSynchronize((cudaStream_t)stream);
+}
+
+GTS_EXPORT int gts_b200_event_create(void** event) {
+  return (int)cudaEventCreate((cudaEvent_t*)event);
+}
+GTS_EXPORT int gts_b200_event_destroy(void* event) {
+  return (int)cudaEventDestroy((cudaEvent_t)event);
+}
+GTS_EXPORT int gts_b200_event_record(void* event, void* stream) {
+  return (int)cudaEventRecord((cudaEvent_t)event, (cudaStream_t)stream);
+}
+GTS_EXPORT int gts_b200_event_synchronize(void* event) {
+  return (int)cudaEventSynchronize((cudaEvent_t)event);
+}
+GTS_EXPORT int gts_b200_event_elapsed_ms(float* ms, void* start, void* end) {
+  return (int)cudaEventElapsedTime(ms, (cudaEvent_t)start, (cudaEvent_t)end);
+}
+
+// ---------------------------------------------------------------------------
+// L2 flush: write 2x L2 bytes with a streaming kernel.
+// ---------------------------------------------------------------------------
+__global__ void gts_flush_kernel(uint4* p, size_t n, unsigned salt) {
+  size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (; t < n; t += stride) p[t] = make_uint4(salt, (unsigned)t, salt ^ 0x9e3779b9u, 0u);
+}
+
+static std::mutex g_flush_mu;
+static void* g_flush_buf[64];
+static size_t g_flush_bytes[64];
+static unsigned g_flush_salt = 1;
+
+GTS_EXPORT int gts_b200_l2_flush(void* stream) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return (int)e;
+  if (dev < 0 || dev >= 64) return (int)cudaErrorInvalidDevice;
+  std::lock_guard<std::mutex> lock(g_flush_mu);
+  if (!g_flush_buf[dev]) {
+    int l2 = 0;
+    e = cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
+    if (e != cudaSuccess) return (int)e;
+    size_t bytes = (size_t)(l2 > 0 ? l2 : (128 << 20)) * 2;
+    e = cudaMalloc(&g_flush_buf[dev], bytes);
+    if (e != cudaSuccess) return (int)e;
+    g_flush_bytes[dev] = bytes;
+  }
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const size_t n = g_flush_bytes[dev] / sizeof(uint4);
+  gts_flush_kernel<<<sms * 4, 512, 0, (cudaStream_t)stream>>>((uint4*)g_flush_buf[dev], n,
+                                                               g_flush_salt++);
+  return (int)cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Halo pack / unpack (3-D strided box <-> contiguous (k, i, j) buffer).
+// ---------------------------------------------------------------------------
+template <typename T, bool kPack>
+__global__ void gts_box_kernel(T* buf, T* base, int64_t s_i, int64_t s_j, int64_t s_k,
+                               int64_t i0, int64_t j0, int64_t k0, int64_t ni, int64_t nj,
+                               int64_t nk) {
+  const int64_t n = ni * nj * nk;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = t % nj;
+    const int64_t r = t / nj;
+    const int64_t i = r % ni;
+    const int64_t k = r / ni;
+    T* g = base + (i0 + i) * s_i + (j0 + j) * s_j + (k0 + k) * s_k;
+    if (kPack)
+      buf[t] = *g;
+    else
+      *g = buf[t];
+  }
+}
+
+template <bool kPack>
+static int box(void* buf, const void* base, int64_t s_i, int64_t s_j, int64_t s_k, int64_t i0,
+               int64_t j0, int64_t k0, int64_t ni, int64_t nj, int64_t nk, int itemsize,
+               void* stream) {
+  const int64_t n = ni * nj * nk;
+  if (n <= 0) return 0;
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (itemsize == 8)
+    gts_box_kernel<unsigned long long, kPack><<<(unsigned)blocks, 256, 0, st>>>(
+        (unsigned long long*)buf, (unsigned long long*)base, s_i, s_j, s_k, i0, j0, k0, ni, nj,
+        nk);
+  else if (itemsize == 4)
+    gts_box_kernel<unsigned int, kPack><<<(unsigned)blocks, 256, 0, st>>>(
+        (unsigned int*)buf, (unsigned int*)base, s_i, s_j, s_k, i0, j0, k0, ni, nj, nk);
+  else
+    return (int)cudaErrorInvalidValue;
+  return (int)cudaGetLastError();
+}
+
+GTS_EXPORT int gts_b200_pack_box(void* buf, const void* base, int64_t s_i, int64_t s_j,
+                                 int64_t s_k, int64_t i0, int64_t j0, int64_t k0, int64_t ni,
+                                 int64_t nj, int64_t nk, int itemsize, void* stream) {
+  return box<true>(buf, base, s_i, s_j, s_k, i0, j0, k0, ni, nj, nk, itemsize, stream);
+}
+GTS_EXPORT int gts_b200_unpack_box(void* base, const void* buf, int64_t s_i, int64_t s_j,
+                                   int64_t s_k, int64_t i0, int64_t j0, int64_t k0, int64_t ni,
+                                   int64_t nj, int64_t nk, int itemsize, void* stream) {
+  return box<false>((void*)buf, base, s_i, s_j, s_k, i0, j0, k0, ni, nj, nk, itemsize, stream);
+}
