@@ -1,0 +1,468 @@
+#!/usr/bin/env python
+"""Benchmark: grid-points/s and achieved HBM GB/s of the b200 stencil backend.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+One JSON line on rank 0.  A "step" = one call of the stencil over the whole
+configured domain.  Default workload (N=1) = BASELINE.json configs[1],
+vertical advection 256x256x80 float64; hdiff 256x256x80 f64/f32 (configs[2])
+are measured on the same run and reported under "extra".  For N>1 every rank
+runs its own 256x256x80 shard (weak scaling; vadv columns are independent, no
+data-path collective).
+
+Protocol: inputs resident in HBM; R >= 3 rotating
+input/output sets whose total exceeds 2x L2, so consecutive steps never hit
+their own data in L2; W warm-up steps; K timed steps bracketed by
+barrier + device synchronise; CUDA events on the launching stream; max over
+ranks.  "e2e" = the same metric through the reference-facing API
+(CompiledStencil.__call__) with host FieldStorages in pinned memory, the
+host<->device copies inside the timed region.  "cpu_baseline" = the
+reference's own native kernel (the C its gen engine emits, oracle/_ref) timed
+on this host's cores on a bounded sample.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+REPO = Path(__file__).resolve().parent
+sys.path.insert(0, str(REPO))
+
+WORKLOADS = {
+    # name: (kernel, dtype, domain)
+    "vadv": ("vadv", "f64", (256, 256, 80)),
+    "hdiff": ("hdiff", "f64", (256, 256, 80)),
+    "hdiff32": ("hdiff", "f32", (256, 256, 80)),
+    "vadv32": ("vadv", "f32", (256, 256, 80)),
+}
+CONFIG_TEXT = {
+    "vadv": "vertical advection (FORWARD/BACKWARD Thomas) 256x256x80 float64",
+    "hdiff": "horizontal diffusion 256x256x80 float64",
+    "hdiff32": "horizontal diffusion 256x256x80 float32",
+    "vadv32": "vertical advection 256x256x80 float32",
+}
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=1000)
+    p.add_argument("--warmup", type=int, default=20)
+    p.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    p.add_argument("--workload", default="vadv", choices=sorted(WORKLOADS))
+    p.add_argument("--e2e-steps", type=int, default=20)
+    p.add_argument("--cpu-seconds", type=float, default=12.0)
+    p.add_argument("--no-extra", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    return p.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# distributed plumbing (torch.distributed only for barrier / max-reduce)
+# ---------------------------------------------------------------------------
+class Dist:
+    def __init__(self):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = None
+        if self.world > 1:
+            import torch
+            import torch.distributed as dist
+
+            backend = "nccl" if torch.cuda.is_available() else "gloo"
+            if backend == "nccl":
+                torch.cuda.set_device(self.local)
+            dist.init_process_group(backend=backend)
+            self.dist, self.torch, self.backend = dist, torch, backend
+
+    def barrier(self):
+        if self.world > 1:
+            if self.backend == "nccl":
+                self.dist.barrier(device_ids=[self.local])
+            else:
+                self.dist.barrier()
+
+    def max(self, v: float) -> float:
+        if self.world == 1:
+            return v
+        dev = f"cuda:{self.local}" if self.backend == "nccl" else "cpu"
+        t = self.torch.tensor([v], dtype=self.torch.float64, device=dev)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def close(self):
+        if self.world > 1:
+            self.dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region (NVML)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    REASONS = {
+        "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4,
+        "hw_slowdown": 0x8, "sync_boost": 0x10, "sw_thermal_slowdown": 0x20,
+        "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80,
+    }
+
+    def __init__(self, device: int):
+        self.samples, self.reasons = [], set()
+        self.ok = False
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for name, bit in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.ok:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons)}
+        busy = [s for s in self.samples if s > 0]
+        return {"sm_mhz": float(statistics.median(busy or self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons - {"gpu_idle"}), "samples": len(self.samples)}
+
+
+def host_info():
+    model = ""
+    try:
+        for ln in Path("/proc/cpuinfo").read_text().splitlines():
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return os.cpu_count() or 1, model
+
+
+# ---------------------------------------------------------------------------
+# reference CPU implementation (oracle/_ref = the gen engine's own C kernels)
+# ---------------------------------------------------------------------------
+def _ref_kernel(key: str):
+    man_path = REPO / "oracle" / "_ref" / "manifest.json"
+    if not man_path.exists():
+        return None
+    man = json.loads(man_path.read_text())[key]
+    lib = ctypes.CDLL(str(REPO / "oracle" / "_ref" / man["so"]))
+    fn = getattr(lib, man["symbol"])
+    nf, ns = len(man["fields"]), len(man["scalars"])
+    fn.argtypes = [ctypes.c_longlong] * 3 + ([ctypes.c_void_p] + [ctypes.c_longlong] * 6) * nf + \
+        [ctypes.c_float if d == "f32" else ctypes.c_double for _, d in man["scalars"]]
+    fn.restype = None
+    return fn, man
+
+
+def _ref_args(kernel, dtype, domain, seed=0):
+    """Reference inputs in the gen layout (reference harness builders)."""
+    import paper_2311_08322_b200  # noqa: F401  (locates stencilforge)
+    import stencilforge as sf
+    from stencilforge import bench as sf_bench
+
+    args = sf_bench.KERNEL_BUILDERS[kernel]("gen", tuple(domain), seed)
+    if dtype == "f32":
+        for n, v in list(args.items()):
+            if isinstance(v, sf.FieldStorage):
+                st = sf.allocate("f32", tuple(d - 2 * o for d, o in zip(v.shape, v.origin)), v.origin, v.layout)
+                st.view[...] = v.view.astype(np.float32)
+                args[n] = st
+    return args
+
+
+def time_reference(kernel, dtype, domain, seconds: float, max_calls: int, warmup: int = 3):
+    """Time the reference gen kernel on all host cores; returns (s per call, calls, kind)."""
+    got = _ref_kernel(f"{kernel}_{dtype}")
+    if got is None:
+        return None
+    fn, man = got
+    args = _ref_args(kernel, dtype, domain)
+    call = [int(domain[0]), int(domain[1]), int(domain[2])]
+    for n in man["fields"]:
+        st = args[n]
+        call += [st.base_address(), *st.strides, *st.origin]
+    for n, _ in man["scalars"]:
+        call.append(float(args[n]))
+    for _ in range(warmup):
+        fn(*call)
+    times = []
+    t_end = time.perf_counter() + seconds
+    while len(times) < max_calls and (not times or time.perf_counter() < t_end):
+        t0 = time.perf_counter()
+        fn(*call)
+        times.append(time.perf_counter() - t0)
+    return times
+
+
+def run_reference(args, dist):
+    if dist.rank != 0:
+        return
+    kernel, dtype, domain = WORKLOADS[args.workload]
+    pts = domain[0] * domain[1] * domain[2]
+    cores, model = host_info()
+    times = time_reference(kernel, dtype, domain, seconds=150.0, max_calls=args.steps,
+                           warmup=max(args.warmup, 1))
+    if times is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built (run __graft_entry__.build() in the build container)"}))
+        return
+    total = sum(times)
+    value = pts * len(times) / total
+    line = {
+        "metric": "grid-points/s", "value": value, "unit": "grid-points/s", "impl": "reference",
+        "n_gpus": args.gpus, "steps": len(times), "warmup": args.warmup,
+        "ms_per_step": total / len(times) * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": dtype, "data": "synthetic",
+        "config": {"workload": CONFIG_TEXT[args.workload], "domain": list(domain), "parallelism": "openmp"},
+        "cpu_baseline": {"value": value, "unit": "grid-points/s", "cores": cores, "kind": "reference",
+                         "sample": f"{len(times)} full-domain calls of the reference gen engine's "
+                                   f"generated C kernel (oracle/_ref, -O3 -fopenmp -ffp-contract=off), "
+                                   f"OpenMP over all {cores} host threads ({model})"},
+        "e2e": {"value": value, "unit": "grid-points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+# ---------------------------------------------------------------------------
+# b200
+# ---------------------------------------------------------------------------
+def measured_peak():
+    p = REPO / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            return float(json.loads(p.read_text())["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+        except Exception:
+            pass
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(workload: str):
+    p = REPO / "profiles" / "ncu_traffic.json"
+    if p.exists():
+        try:
+            return json.loads(p.read_text()).get(workload)
+        except Exception:
+            return None
+    return None
+
+
+def device_timed(st, kernel, dtype, domain, steps, warmup, dist, sampler=None):
+    """Device-resident timing with rotating buffer sets."""
+    from paper_2311_08322_b200 import native, workloads
+
+    info = native.device_info()
+    set_bytes = workloads.algorithmic_bytes(kernel, domain, dtype)
+    nsets = max(3, -(-(3 * info["l2_bytes"]) // max(set_bytes, 1)))
+    nsets = min(nsets, 16)
+    stream = native.default_stream()
+    module = st.build_info["module"]
+    sets, launchers = [], []
+    for s in range(nsets):
+        a = workloads.make_args(kernel, domain, dtype, seed=s)
+        sets.append(a)
+        fields = {k: v for k, v in a.items() if hasattr(v, "base_address")}
+        scal = {k: v for k, v in a.items() if not hasattr(v, "base_address")}
+        launchers.append(module.launcher(domain, fields, scal, stream))
+    for i in range(warmup):
+        launchers[i % nsets]()
+    native.synchronize(stream)
+    ev = [(native.Event(), native.Event()) for _ in range(steps)]
+    e0, e1 = native.Event(), native.Event()
+    dist.barrier()
+    native.synchronize(stream)
+    ctx = sampler if sampler is not None else _Null()
+    with ctx:
+        e0.record(stream)
+        for i in range(steps):
+            ev[i][0].record(stream)
+            launchers[(warmup + i) % nsets]()
+            ev[i][1].record(stream)
+        e1.record(stream)
+        native.synchronize(stream)
+    dist.barrier()
+    total_ms = e0.elapsed_ms(e1)
+    launch_ms = [a.elapsed_ms(b) for a, b in ev]
+    return {"total_ms": total_ms, "launch_ms_mean": statistics.fmean(launch_ms),
+            "launch_ms_median": statistics.median(launch_ms), "nsets": nsets,
+            "set_mb": set_bytes / 1e6, "l2_mb": info["l2_bytes"] / 1e6, "sets": sets,
+            "launches_per_step": sum(1 for k in module.plan.kernels)}
+
+
+class _Null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
+def parity_check(kernel, dtype, sets):
+    """Verify the last buffer set against the C oracle (bitwise)."""
+    sys.path.insert(0, str(REPO / "oracle"))
+    import oracle
+
+    a = sets[0]
+    if kernel == "hdiff":
+        want = oracle.hdiff_c(a["inp"].host_array(), a["coeff"])
+        got = a["out"].host_array()
+    else:
+        want = oracle.vadv_c(*[a[n].host_array() for n in "abcd"])
+        got = a["x"].host_array()
+    return "bitwise" if np.array_equal(got, want) else f"max_rel {oracle.max_rel(got, want):.3e}"
+
+
+def e2e_timed(st, kernel, dtype, domain, steps):
+    """Through CompiledStencil.__call__ with pinned host FieldStorages."""
+    from paper_2311_08322_b200 import storage as b2s
+    from paper_2311_08322_b200 import workloads
+
+    host = workloads.make_args(kernel, domain, dtype, device=False)
+    args = {}
+    for n, v in host.items():
+        if hasattr(v, "base_address"):
+            halo = v.origin
+            comp = tuple(s - 2 * h for s, h in zip(v.shape, halo))
+            p = b2s.pinned_host_storage(v.dtype, comp, halo)
+            p.view[...] = v.view
+            args[n] = p
+        else:
+            args[n] = v
+    module = st.build_info["module"]
+    h2d = sum(v._base.nbytes for v in args.values() if hasattr(v, "base_address"))
+    d2h = sum(args[n]._base.nbytes for n in module.written)
+    st(**args)  # warm (allocates the device mirrors)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        st(**args)
+    dt = (time.perf_counter() - t0) / steps
+    return dt, h2d, d2h
+
+
+def run_b200(args, dist):
+    import paper_2311_08322_b200 as b200
+    from paper_2311_08322_b200 import native, workloads
+
+    if dist.world > 1:
+        native.set_device(dist.local)
+    dev = native.require_device()
+    kernel, dtype, domain = WORKLOADS[args.workload]
+    st = b200.compile_stencil(workloads.source(kernel, dtype), kernel)
+    pts = domain[0] * domain[1] * domain[2]
+    sampler = ClockSampler(dev)
+    r = device_timed(st, kernel, dtype, domain, args.steps, args.warmup, dist, sampler)
+    total_ms = dist.max(r["total_ms"])
+    launch_ms = dist.max(r["launch_ms_mean"])
+    ms_per_step = total_ms / args.steps
+    value = dist.world * pts / (ms_per_step / 1e3)
+    parity = parity_check(kernel, dtype, r["sets"])
+    del r["sets"]
+    peak, peak_src = measured_peak()
+    alg = workloads.algorithmic_bytes(kernel, domain, dtype)
+    achieved = alg / (launch_ms / 1e3) / 1e9
+    e2e_s, h2d, d2h = e2e_timed(st, kernel, dtype, domain, args.e2e_steps)
+    e2e_val = dist.max(e2e_s)
+    line = {
+        "metric": "grid-points/s (achieved HBM GB/s in roofline)",
+        "value": value, "unit": "grid-points/s", "n_gpus": dist.world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": dtype,
+        "data": "synthetic (reference bench generators, seeds 0..R-1)",
+        "config": {"workload": CONFIG_TEXT[args.workload], "domain_per_gpu": list(domain),
+                   "parallelism": f"independent column shards x{dist.world}" if dist.world > 1 else "single GPU",
+                   "l2": f"{r['nsets']} rotating input/output sets of {r['set_mb']:.0f} MB "
+                         f"(> 2x the {r['l2_mb']:.0f} MB L2)"},
+        "parity": parity,
+        "e2e": {"value": dist.world * pts / e2e_val, "unit": "grid-points/s",
+                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                "ms_per_step": e2e_val * 1e3,
+                "path": "CompiledStencil.__call__ with host FieldStorages (pinned), mirror mode"},
+        "gpu_launches": args.steps * r["launches_per_step"],
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": ncu_traffic(args.workload),
+                     "algorithmic_bytes_per_launch": alg, "kernel_ms_mean": launch_ms,
+                     "peak_source": peak_src, "frac_of_8TBs_spec": achieved / 8000.0},
+        "clocks": sampler.summary(),
+    }
+    if dist.rank == 0 and dist.world == 1 and not args.no_extra:
+        extra = {}
+        for name in ("hdiff", "hdiff32"):
+            k2, d2, dom2 = WORKLOADS[name]
+            st2 = b200.compile_stencil(workloads.source(k2, d2), k2)
+            r2 = device_timed(st2, k2, d2, dom2, max(args.steps // 2, 50), args.warmup, dist)
+            alg2 = workloads.algorithmic_bytes(k2, dom2, d2)
+            ach2 = alg2 / (r2["launch_ms_mean"] / 1e3) / 1e9
+            extra[name] = {
+                "workload": CONFIG_TEXT[name],
+                "value": dom2[0] * dom2[1] * dom2[2] / (r2["total_ms"] / max(args.steps // 2, 50) / 1e3),
+                "unit": "grid-points/s", "ms_per_step": r2["total_ms"] / max(args.steps // 2, 50),
+                "kernel_ms_mean": r2["launch_ms_mean"], "achieved_gbs": ach2, "frac": ach2 / peak,
+                "parity": parity_check(k2, d2, r2["sets"]), "traffic": ncu_traffic(name),
+                "launches_per_step": r2["launches_per_step"],
+            }
+        line["extra"] = extra
+    if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
+        cores, model = host_info()
+        times = time_reference(kernel, dtype, domain, seconds=args.cpu_seconds, max_calls=100000)
+        if times:
+            v = pts / statistics.median(times)
+            line["cpu_baseline"] = {
+                "value": v, "unit": "grid-points/s", "cores": cores, "kind": "reference",
+                "sample": f"{len(times)} full {domain[0]}x{domain[1]}x{domain[2]} calls (median) of the "
+                          f"reference gen engine's own generated C kernel (oracle/_ref), OpenMP over "
+                          f"{cores} host threads ({model}), ~{args.cpu_seconds:.0f} s",
+            }
+    if dist.rank == 0:
+        print(json.dumps(line))
+
+
+def main():
+    args = parse()
+    dist = Dist()
+    try:
+        if args.impl == "reference":
+            run_reference(args, dist)
+        else:
+            run_b200(args, dist)
+    finally:
+        dist.close()
+
+
+if __name__ == "__main__":
+    main()

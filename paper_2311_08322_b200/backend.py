@@ -102,6 +102,35 @@ class Module:
             native.check(self.lib.gts_b200_module_set_device(dev), "module set device")
             self._device = dev
 
+    def launcher(self, domain, fields: dict, scalars: dict, stream: int):
+        """Pre-marshalled asynchronous launch over device-resident storages
+        ({name: DeviceFieldStorage}, origins = storage origins).  Returns a
+        zero-argument callable: one call = one enqueue of the stencil."""
+        self.bind_device()
+        args: list = [int(domain[0]), int(domain[1]), int(domain[2])]
+        for name in self.field_order:
+            st = fields[name]
+            if not isinstance(st, DeviceFieldStorage):
+                raise TypeError(f"launcher needs device-resident fields; '{name}' is {type(st).__name__}")
+            st.to_device(stream)
+            args.append(st.base_address())
+            args.extend(int(s) for s in st.strides)
+            args.extend(int(o) for o in st.origin)
+        for name in self.scalar_order:
+            args.append(float(scalars[name]))
+        args.append(stream)
+        fn, sym = self.fn, self.symbol
+        written = [fields[n] for n in self.written]
+
+        def go() -> None:
+            status = fn(*args)
+            if status:
+                raise native.DeviceError(status, sym)
+            for w in written:
+                w._device_dirty = True
+
+        return go
+
     def launch(self, domain, pointers: dict, strides: dict, origins: dict, scalars: dict,
                stream: int) -> None:
         """Asynchronous launch with raw device pointers (no copies, no sync)."""

@@ -295,7 +295,9 @@ def _point_kernel(kname: str, stage, ctype: dict, dtypes: dict) -> list:
 
 def generate_source(plan: Plan, fp, options: Optional[dict] = None) -> str:
     impl = plan.impl
-    from . import codegen_parallel  # fused PARALLEL template instantiation
+    from . import codegen_column, codegen_parallel  # template instantiations
+
+    opts = options or {}
 
     ct = {ir.F32: "float", ir.F64: "double"}
     dtypes = {f.name: f.dtype for f in impl.api_fields}
@@ -309,6 +311,7 @@ def generate_source(plan: Plan, fp, options: Optional[dict] = None) -> str:
     w(f"// stencil: {impl.name}  fingerprint: {fp.digest}")
     w(f"// plan: {' '.join(plan.describe())}")
     w('#include "gts_common.cuh"')
+    w('#include "gts_sm100.cuh"')
     if any(k.kind == "pfused" for k in plan.kernels):
         w('#include "gts_parallel.cuh"')
     w("")
@@ -374,6 +377,12 @@ def generate_source(plan: Plan, fp, options: Optional[dict] = None) -> str:
             launches.append("  }")
         elif k.kind == "column":
             out.extend(_column_kernel(kname, plan, k, ctype, dtypes))
+            sp = codegen_column.spec(plan, k, dtypes) if opts.get("tmem", True) else None
+            if sp is not None:
+                code, launch = codegen_column.emit(kname, plan, k, sp, ctype, dtypes)
+                out.extend(code)
+                launches += launch
+                continue
             launches += [
                 "  {",
                 "    dim3 grid((unsigned)((nj + GTS_COL_TJ - 1) / GTS_COL_TJ),"

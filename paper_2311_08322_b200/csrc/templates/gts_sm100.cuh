@@ -1,0 +1,189 @@
+// gts_sm100.cuh -- sm_100a building blocks used by the stencil templates:
+// mbarriers, TMA tensor loads (cp.async.bulk.tensor), Tensor Memory
+// (tcgen05.alloc / st / ld) and host-side tensor-map encoding through the
+// driver entry point (no libcuda link needed).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+// ---------------------------------------------------------------------------
+// mbarrier
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t gts_smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void gts_mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(gts_smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void gts_fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void gts_mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(gts_smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void gts_mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(gts_smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void gts_mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = gts_smem_u32(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+
+// Generic-proxy reads of a smem buffer must be ordered before the async
+// proxy (TMA) overwrites it.
+__device__ __forceinline__ void gts_fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// ---------------------------------------------------------------------------
+// TMA
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void gts_tma_load_3d(void* smem_dst, const CUtensorMap* map,
+                                                uint64_t* bar, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(gts_smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(gts_smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
+__device__ __forceinline__ void gts_prefetch_tensormap(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// Tensor Memory (TMEM): 128 lanes x 512 columns x 32 bit per SM.  Warp w of
+// the CTA owns lanes 32*(w%4) .. 32*(w%4)+31; with 32x32b shapes thread t of
+// the warp reads / writes its own lane.
+// ---------------------------------------------------------------------------
+template <int kCols>
+__device__ __forceinline__ void gts_tmem_alloc(uint32_t* smem_addr_slot) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                   gts_smem_u32(smem_addr_slot)),
+               "n"(kCols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+
+template <int kCols>
+__device__ __forceinline__ void gts_tmem_dealloc(uint32_t taddr) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(kCols)
+               : "memory");
+}
+
+__device__ __forceinline__ void gts_tmem_fence_before_sync() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void gts_tmem_fence_after_sync() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+__device__ __forceinline__ void gts_tmem_st2(uint32_t taddr, uint32_t r0, uint32_t r1) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};" ::"r"(taddr), "r"(r0),
+               "r"(r1)
+               : "memory");
+}
+__device__ __forceinline__ void gts_tmem_st1(uint32_t taddr, uint32_t r0) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(taddr), "r"(r0)
+               : "memory");
+}
+__device__ __forceinline__ void gts_tmem_wait_st() {
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ void gts_tmem_ld2(uint32_t taddr, uint32_t& r0, uint32_t& r1) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];"
+               : "=r"(r0), "=r"(r1)
+               : "r"(taddr)
+               : "memory");
+}
+__device__ __forceinline__ void gts_tmem_ld1(uint32_t taddr, uint32_t& r0) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];"
+               : "=r"(r0)
+               : "r"(taddr)
+               : "memory");
+}
+__device__ __forceinline__ void gts_tmem_wait_ld() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ void gts_tmem_store_f64(uint32_t taddr, double v) {
+  gts_tmem_st2(taddr, (uint32_t)__double2loint(v), (uint32_t)__double2hiint(v));
+}
+__device__ __forceinline__ void gts_tmem_store_f32(uint32_t taddr, float v) {
+  gts_tmem_st1(taddr, __float_as_uint(v));
+}
+
+// ---------------------------------------------------------------------------
+// Host: tensor maps
+// ---------------------------------------------------------------------------
+typedef CUresult (*gts_encode_tiled_fn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                        const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                        const cuuint32_t*, CUtensorMapInterleave,
+                                        CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                        CUtensorMapFloatOOBfill);
+
+static gts_encode_tiled_fn gts_get_encode_tiled() {
+  static gts_encode_tiled_fn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (gts_encode_tiled_fn)p;
+  }
+  return fn;
+}
+
+// 3-D tiled map over a field with j contiguous: dims {nj, ni, nk}, element
+// strides {1, s_i, s_k}; ``origin`` points at element (0, 0, 0) of the box
+// coordinate system.  Returns false when the field is not TMA-compatible
+// (16-B aligned base and byte strides) -- the caller then uses the
+// non-TMA kernel.
+static bool gts_make_tmap_3d(CUtensorMap* map, const void* origin, int itemsize, long long nj,
+                             long long ni, long long nk, long long s_i, long long s_j,
+                             long long s_k, unsigned bj, unsigned bi, unsigned bk) {
+  gts_encode_tiled_fn enc = gts_get_encode_tiled();
+  if (!enc) return false;
+  if (s_j != 1) return false;
+  if (((uintptr_t)origin) % 16) return false;
+  if ((s_i * itemsize) % 16 || (s_k * itemsize) % 16) return false;
+  if (s_i <= 0 || s_k <= 0) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)nj, (cuuint64_t)ni, (cuuint64_t)nk};
+  cuuint64_t strides[2] = {(cuuint64_t)(s_i * itemsize), (cuuint64_t)(s_k * itemsize)};
+  cuuint32_t box[3] = {bj, bi, bk};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(map, itemsize == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                   3, const_cast<void*>(origin), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+static int gts_sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}

@@ -225,3 +225,44 @@ def to_device(storage: FieldStorage) -> DeviceFieldStorage:
     st._host_view[...] = storage.view
     st.to_device()
     return st
+
+
+class _PinnedHost:
+    """Owning pinned host allocation backing a host FieldStorage."""
+
+    def __init__(self, nbytes: int):
+        h = ctypes.c_void_p()
+        native.call("gts_b200_host_alloc", ctypes.byref(h), int(nbytes))
+        self.hptr = h.value
+        self._fin = weakref.finalize(self, _PinnedHost._release, self.hptr)
+
+    @staticmethod
+    def _release(hptr):  # pragma: no cover - GC path
+        try:
+            native.lib().gts_b200_host_free(hptr)
+        except Exception:
+            pass
+
+
+def pinned_host_storage(dtype: str, compute_shape, halo=(0, 0, 0),
+                        layout: Optional[LayoutSpec] = None) -> FieldStorage:
+    """A plain reference FieldStorage (host, storage.py:74-103) whose buffer
+    is page-locked, so mirror-mode copies run at full PCIe/C2C speed."""
+    layout = layout or B200_LAYOUT
+    np_dtype = _NP[dtype]
+    shape = tuple(c + 2 * h for c, h in zip(compute_shape, halo))
+    strides, total = _strides(shape, layout, np_dtype.itemsize)
+    slack = layout.alignment_bytes // np_dtype.itemsize
+    owner = _PinnedHost((total + slack) * np_dtype.itemsize)
+    raw = (ctypes.c_char * ((total + slack) * np_dtype.itemsize)).from_address(owner.hptr)
+    base = np.frombuffer(raw, dtype=np_dtype)
+    origin_linear = sum(o * s for o, s in zip(halo, strides))
+    shift = ((-(owner.hptr + origin_linear * np_dtype.itemsize)) % layout.alignment_bytes) // np_dtype.itemsize
+    view = np.lib.stride_tricks.as_strided(
+        base[shift: shift + total], shape=shape,
+        strides=tuple(s * np_dtype.itemsize for s in strides))
+    view[...] = 0
+    st = FieldStorage(dtype=dtype, shape=shape, origin=tuple(halo), layout=layout,
+                      strides=strides, view=view, _base=base)
+    st._pinned_owner = owner  # keep the allocation alive with the storage
+    return st

@@ -74,8 +74,23 @@ def toolchain_version() -> str:
         raise BackendError(Code.TOOLCHAIN_MISSING, f"'{nvcc} --version' failed: {out.stderr.strip()}")
     release = [ln for ln in out.stdout.splitlines() if "release" in ln]
     version = release[0].strip() if release else out.stdout.strip().splitlines()[-1]
-    _PROBE[nvcc] = f"nvcc | {version} | sm_100a | {' '.join(compile_flags())}"
+    _PROBE[nvcc] = (f"nvcc | {version} | sm_100a | {' '.join(compile_flags())} | "
+                    f"codegen {codegen_digest()}")
     return _PROBE[nvcc]
+
+
+def codegen_digest() -> str:
+    """Content hash of the lowering, code generators and templates: part of
+    the toolchain string, so a generator change can never serve a stale
+    module from the cache."""
+    import hashlib
+
+    h = hashlib.sha256()
+    files = sorted(PKG.glob("codegen*.py")) + [PKG / "lowering.py"] + sorted(TEMPLATES.glob("*.cuh"))
+    for f in files:
+        h.update(f.name.encode())
+        h.update(f.read_bytes())
+    return h.hexdigest()[:12]
 
 
 def _invoke_nvcc(src: Path, so: Path) -> None:
