@@ -62,8 +62,48 @@ def entry_name(impl, fp) -> str:
     return f"gts_run_{impl.name}_{fp.short}"
 
 
+class DivPool:
+    """Shared-reciprocal division (``gts_rcp`` / ``gts_div`` in
+    gts_common.cuh): every distinct denominator is refined once per scope and
+    reused by later quotients over the same value (vadv divides cp's and
+    dp's numerators by the same ``b - a*cp[k-1]``, vadv.gts:10-12).  Results
+    stay bitwise the IEEE quotient."""
+
+    def __init__(self, mode: str = "branch"):
+        self.map: dict = {}
+        self.pending: list = []
+        self.depth = 0
+        self.n = 0
+        # "branch": gts_div (exact, per-quotient slow-path branch)
+        # "fast":   gts_div_fast, sets the kernel's bad_ flag (replayed exactly)
+        # "exact":  plain IEEE division
+        self.mode = mode
+
+    def rcp(self, den: str) -> str:
+        if den in self.map:
+            return self.map[den]
+        var = f"rcp{self.n}"
+        self.n += 1
+        self.pending.append(f"const GtsRcp {var} = gts_rcp({den});")
+        if self.depth == 0:
+            self.map[den] = var
+        return var
+
+    def flush(self, indent: str, out: list) -> None:
+        for ln in self.pending:
+            out.append(indent + ln)
+        self.pending = []
+
+    def invalidate(self, field: str) -> None:
+        keys = [k for k in self.map if f"cur_{field}" in k or f"p.f_{field}," in k]
+        for k in keys:
+            del self.map[k]
+
+
 class _Ctx:
     """How a field access at an offset is spelled inside one kernel."""
+
+    pool = None  # optional DivPool
 
     def __init__(self, dtypes: dict):
         self.dtypes = dtypes  # name -> "f32" | "f64"
@@ -101,6 +141,12 @@ def emit_expr(e, ctx: _Ctx) -> str:
         inner = emit_expr(e.operand, ctx)
         return f"(!{inner})" if e.op == "not" else f"(-{inner})"
     if isinstance(e, ir.BinaryOp):
+        if e.op == "/" and ctx.pool is not None and ctx.pool.mode != "exact":
+            num = emit_expr(e.left, ctx)
+            rcp = ctx.pool.rcp(emit_expr(e.right, ctx))
+            if ctx.pool.mode == "fast":
+                return f"gts_div_fast({num}, {rcp}, bad_)"
+            return f"gts_div({num}, {rcp})"
         op = _BINOP.get(e.op, e.op)
         return f"({emit_expr(e.left, ctx)} {op} {emit_expr(e.right, ctx)})"
     if isinstance(e, ir.BuiltinCall):
@@ -120,24 +166,34 @@ def _store_mem(name: str, value: str, ctx: _MemCtx, ctype: dict) -> str:
 
 def emit_stmt_mem(stmt, ctx: _MemCtx, ctype: dict, indent: str, out: list,
                   on_write=None) -> None:
+    if ctx.pool is None:
+        ctx.pool = DivPool()
+    pool = ctx.pool
     if isinstance(stmt, ir.Assign):
         name = stmt.target.field
-        out.append(f"{indent}{{ const double v_ = {emit_expr(stmt.value, ctx)};")
+        value = emit_expr(stmt.value, ctx)
+        pool.flush(indent, out)
+        out.append(f"{indent}{{ const double v_ = {value};")
         out.append(f"{indent}  {_store_mem(name, 'v_', ctx, ctype)}")
         if on_write is not None:
             extra = on_write(name, "v_")
             if extra:
                 out.append(f"{indent}  {extra}")
         out.append(f"{indent}}}")
+        pool.invalidate(name)
         return
     if isinstance(stmt, ir.If):
-        out.append(f"{indent}if ({emit_expr(stmt.cond, ctx)}) {{")
+        cond = emit_expr(stmt.cond, ctx)
+        pool.flush(indent, out)
+        out.append(f"{indent}if ({cond}) {{")
+        pool.depth += 1
         for s in stmt.then_body:
             emit_stmt_mem(s, ctx, ctype, indent + "  ", out, on_write)
         if stmt.else_body:
             out.append(f"{indent}}} else {{")
             for s in stmt.else_body:
                 emit_stmt_mem(s, ctx, ctype, indent + "  ", out, on_write)
+        pool.depth -= 1
         out.append(f"{indent}}}")
         return
     raise TypeError(f"cannot generate code for {type(stmt).__name__}")
@@ -244,6 +300,7 @@ def _column_kernel(kname: str, plan: Plan, kplan, ctype: dict, dtypes: dict) -> 
                     return f"cur_{name} = (double)({ctype[name]})({v});"
                 return ""
 
+            ctx.pool = DivPool()
             for st in stages:
                 emit_stmt_mem(st.body, ctx, ctype, "          ", out, on_write)
             for f, depth in sorted(cached.items()):
@@ -379,7 +436,7 @@ def generate_source(plan: Plan, fp, options: Optional[dict] = None) -> str:
             out.extend(_column_kernel(kname, plan, k, ctype, dtypes))
             sp = codegen_column.spec(plan, k, dtypes) if opts.get("tmem", True) else None
             if sp is not None:
-                code, launch = codegen_column.emit(kname, plan, k, sp, ctype, dtypes)
+                code, launch = codegen_column.emit(kname, plan, k, sp, ctype, dtypes, opts)
                 out.extend(code)
                 launches += launch
                 continue

@@ -33,13 +33,14 @@ from dataclasses import dataclass
 from typing import Optional
 
 from ._host import ir
-from .codegen import _bound, _interval_groups, _MemCtx, c_float, emit_expr  # noqa: F401
+from .codegen import DivPool, _bound, _interval_groups, _MemCtx, c_float, emit_expr  # noqa: F401
 from .lowering import always_writes, reads, writes
 
-KB = 8  # levels per TMA box
-TI, TJ = 4, 32  # tile: 4 rows (one per consumer warp) x 32 contiguous columns
+KB = 8  # levels per TMA box (W=1 variant)
+TI, TJ = 4, 32  # tile rows per consumer-warp group x 32 contiguous columns
 RING_BUDGET = 196 * 1024
 MAX_STAGES = 8
+SMEM_MAX = 232448  # max dynamic shared memory per CTA on sm_100a
 
 
 @dataclass
@@ -121,6 +122,8 @@ class _Ctx(_MemCtx):
     def __init__(self, dtypes, sp: ThomasSpec, phase: str, cached: dict, ctype: dict):
         super().__init__(dtypes)
         self.sp, self.phase, self.cached, self.ctype = sp, phase, cached, ctype
+        self.ring = True  # forward reads of streamed fields come from the TMA ring
+        self.div_mode = "fast"
 
     def addr(self, name, off):
         di, dj, dk = off
@@ -130,8 +133,9 @@ class _Ctx(_MemCtx):
         return f"GTS_AT(p.f_{name}, {ii}, {jj}, {kk})"
 
     def read(self, name, off):
-        if self.phase == "f" and name in self.sp.streamed:
-            return f"((double)((const {self.ctype[name]}*)(sb + {self.sp.offs_in_stage[name]}))[(kk * {TI} + warp) * {TJ} + lane])"
+        if self.phase == "f" and self.ring and name in self.sp.streamed:
+            return (f"((double)((const {self.ctype[name]}*)(sb + {self.offs[name]}))"
+                    f"[(kk * {self.rows} + warp) * {TJ} + lane])")
         direction = 1 if self.phase == "f" else -1
         if name in self.cached and not (off[0] or off[1]):
             if off[2] == 0:
@@ -143,23 +147,32 @@ class _Ctx(_MemCtx):
 
 
 def _emit_stmt(stmt, ctx: _Ctx, ctype, api: set, indent: str, out: list) -> None:
+    pool = ctx.pool
     if isinstance(stmt, ir.Assign):
         name = stmt.target.field
-        out.append(f"{indent}{{ const double v_ = {emit_expr(stmt.value, ctx)};")
+        value = emit_expr(stmt.value, ctx)
+        pool.flush(indent, out)
+        out.append(f"{indent}{{ const double v_ = {value};")
         if name in api:
-            out.append(f"{indent}  if (valid) GTS_AT(p.f_{name}, i, j, k) = ({ctype[name]})(v_);")
+            out.append(f"{indent}  {{ {ctype[name]}* xp_ = colp_{name} + (long long)k * p.f_{name}.sk;"
+                       f" if (valid) *xp_ = ({ctype[name]})(v_); }}")
         if name in ctx.cached or name not in api:
             out.append(f"{indent}  cur_{name} = (double)({ctype[name]})(v_);")
         out.append(f"{indent}}}")
+        pool.invalidate(name)
         return
     if isinstance(stmt, ir.If):
-        out.append(f"{indent}if ({emit_expr(stmt.cond, ctx)}) {{")
+        cond = emit_expr(stmt.cond, ctx)
+        pool.flush(indent, out)
+        out.append(f"{indent}if ({cond}) {{")
+        pool.depth += 1
         for s in stmt.then_body:
             _emit_stmt(s, ctx, ctype, api, indent + "  ", out)
         if stmt.else_body:
             out.append(f"{indent}}} else {{")
             for s in stmt.else_body:
                 _emit_stmt(s, ctx, ctype, api, indent + "  ", out)
+        pool.depth -= 1
         out.append(f"{indent}}}")
         return
     raise TypeError(type(stmt).__name__)
@@ -190,27 +203,131 @@ def _need_load(stages, f) -> bool:
     return True
 
 
-def emit(kname: str, plan, kplan, sp: ThomasSpec, ctype: dict, dtypes: dict):
+
+@dataclass
+class Variant:
+    """One launch configuration of the TMEM column template.
+
+    W consumer warps per SM sub-partition (4*W consumer warps, one producer);
+    tile = 4*W rows x 32 columns; the per-column history of the cross
+    temporaries lives in TMEM for the first ``tl`` levels (each thread owns
+    512/W columns of its TMEM lane) and in shared memory for the next ``sl``
+    levels, so the kernel serves any nk <= tl + sl."""
+
+    w: int
+    kb: int
+    nst: int
+    stage_bytes: int
+    offs: dict
+    tl: int
+    sl: int
+    smem_bytes: int
+    hist_off: int
+
+
+def variants(sp: ThomasSpec, dtypes: dict) -> list:
+    esize = {f: (8 if dtypes[f] == ir.F64 else 4) for f in sp.streamed}
+    hist_bytes = 4 * sp.w_level  # bytes per level per column
+    out = []
+    for w, kb, budget in ((2, 4, 128 * 1024), (1, 8, RING_BUDGET)):
+        rows = 4 * w
+        offs, sb = {}, 0
+        for f in sp.streamed:
+            offs[f] = sb
+            sb += kb * rows * TJ * esize[f]
+        nst = max(2, min(MAX_STAGES, budget // sb))
+        ring = nst * sb
+        nct = 32 * rows
+        bars = 2 * 8 * nst + 16
+        free = SMEM_MAX - ring - bars - 64
+        sl = max(0, free // (nct * hist_bytes))
+        hist_off = ring
+        smem = ring + sl * nct * hist_bytes + bars + 16
+        tl = (512 // w) // sp.w_level
+        out.append(Variant(w, kb, nst, sb, offs, tl, sl, smem, hist_off))
+    return out
+
+
+def emit(kname: str, plan, kplan, sp: ThomasSpec, ctype: dict, dtypes: dict, opts=None):
+    code, launch_variants = [], []
+    for v in variants(sp, dtypes):
+        c, cond, call = _emit_variant(kname, plan, sp, v, ctype, dtypes, opts)
+        code += c
+        launch_variants.append((cond, call, v))
+    launch = ["  {"]
+    for f in sp.streamed:
+        launch.append(f"    CUtensorMap tm_{f}[2];")
+    launch.append("    bool launched = false;")
+    for vi, (cond, call, v) in enumerate(launch_variants):
+        launch.append(f"    if (!launched && nk <= {v.tl + v.sl}) {{")
+        launch.append("      bool ok = true;")
+        for f in sp.streamed:
+            e = 8 if dtypes[f] == ir.F64 else 4
+            launch.append(
+                f"      ok = ok && gts_make_tmap_3d(&tm_{f}[{vi}], (const void*)p.f_{f}.p, {e}, nj, ni, nk,"
+                f" p.f_{f}.si, p.f_{f}.sj, p.f_{f}.sk, {TJ}, {4 * v.w}, {v.kb});")
+        launch.append("      if (ok) {")
+        launch += ["        " + ln for ln in call(vi)]
+        launch.append("        launched = true;")
+        launch.append("      }")
+        launch.append("    }")
+    launch += [
+        "    if (!launched) {",
+        "      dim3 grid((unsigned)((nj + GTS_COL_TJ - 1) / GTS_COL_TJ),"
+        " (unsigned)((ni + (GTS_COL_THREADS / GTS_COL_TJ) - 1) / (GTS_COL_THREADS / GTS_COL_TJ)), 1);",
+        f"      {kname}<<<grid, GTS_COL_THREADS, 0, st>>>(p);",
+        "    }",
+        "  }",
+    ]
+    return code, launch
+
+
+def _emit_variant(kname, plan, sp: ThomasSpec, v: Variant, ctype, dtypes, opts):
+    """Persistent warp-specialised kernel: per tile, a FORWARD sweep fed by
+    the TMA ring writes the column history (TMEM tier, then shared-memory
+    tier), then a BACKWARD sweep reads it back.  Each ring stage / history
+    batch is emitted as straight-line code specialised for the interval
+    group and history tier it falls in, so the compiler can overlap the
+    independent work of neighbouring levels with the serial recurrence; a
+    generic per-level-checked body covers partial stages and group
+    boundaries."""
+    dbg = (opts or {}).get("tmem_debug", "")
     impl = plan.impl
     api = {f.name for f in impl.api_fields}
     msf, msb = impl.multistages[sp.ms_f], impl.multistages[sp.ms_b]
+    rows = 4 * v.w
+    ncw = 4 * v.w
+    nct = 32 * ncw
+    threads = nct + 32
+    kn = f"{kname}_tmem_w{v.w}"
+    wl = sp.w_level
+    hb = 4 * wl
+    hoff, o = {}, 0
+    for t in sp.cross:
+        hoff[t] = o
+        o += 4 * sp.words[t] * nct
+    KB = v.kb
+    assert v.tl % KB == 0
     out: list = []
     w = out.append
     tm_params = ", ".join(f"const __grid_constant__ CUtensorMap tm_{f}" for f in sp.streamed)
-    w(f"// TMEM column kernel: streamed {sp.streamed}, TMEM {sp.cross} ({sp.w_level} words/level),"
-      f" ring {sp.nstages} x {sp.stage_bytes} B")
-    w(f"__global__ void __launch_bounds__(160, 1) {kname}_tmem(const __grid_constant__ GtsParams p, "
+    w(f"// TMEM column kernel, W={v.w}: {nct} columns/CTA, streamed {sp.streamed} (ring {v.nst} x"
+      f" {v.stage_bytes} B), history {sp.cross}: TMEM levels [0,{v.tl}), smem levels"
+      f" [{v.tl},{v.tl + v.sl})")
+    w(f"__global__ void __launch_bounds__({threads}, 1) {kn}(const __grid_constant__ GtsParams p, "
       f"{tm_params}, int tiles_j, int ntiles) {{")
     w("  extern __shared__ __align__(1024) unsigned char smem[];")
-    w(f"  constexpr int NST = {sp.nstages};")
-    w(f"  constexpr unsigned STB = {sp.stage_bytes}u;")
-    w("  uint64_t* full = (uint64_t*)(smem + NST * STB);")
+    w(f"  constexpr int NST = {v.nst};")
+    w(f"  constexpr unsigned STB = {v.stage_bytes}u;")
+    w(f"  constexpr int TL = {v.tl};")
+    w(f"  unsigned char* hist = smem + {v.hist_off};")
+    w(f"  uint64_t* full = (uint64_t*)(smem + {v.smem_bytes - (2 * 8 * v.nst + 16) - 16});")
     w("  uint64_t* empty = full + NST;")
     w("  uint32_t* tslot = (uint32_t*)(empty + NST);")
     w("  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;")
     w("  if (warp == 0) gts_tmem_alloc<512>(tslot);")
     w("  if (threadIdx.x == 0) {")
-    w("    for (int s = 0; s < NST; ++s) { gts_mbar_init(&full[s], 1); gts_mbar_init(&empty[s], 4); }")
+    w(f"    for (int s = 0; s < NST; ++s) {{ gts_mbar_init(&full[s], 1); gts_mbar_init(&empty[s], {ncw}); }}")
     w("    gts_fence_mbar_init();")
     w("  }")
     w("  gts_tmem_fence_before_sync();")
@@ -219,27 +336,27 @@ def emit(kname: str, plan, kplan, sp: ThomasSpec, ctype: dict, dtypes: dict):
     w("  const uint32_t tbase = *tslot;")
     w("  const int nk = p.nk;")
     w(f"  const int nkb = (nk + {KB - 1}) / {KB};")
-    w("  if (warp == 4) {")
+    w(f"  if (warp == {ncw}) {{")
     w("    if (lane == 0) {")
     for f in sp.streamed:
         w(f"      gts_prefetch_tensormap(&tm_{f});")
     w("      int it = 0;")
     w("      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {")
-    w(f"        const int j0 = (t % tiles_j) * {TJ}, i0 = (t / tiles_j) * {TI};")
+    w(f"        const int j0 = (t % tiles_j) * {TJ}, i0 = (t / tiles_j) * {rows};")
     w("        for (int kb = 0; kb < nkb; ++kb, ++it) {")
     w("          const int s = it % NST;")
     w("          const uint32_t ph = (uint32_t)(it / NST) & 1u;")
-    w("          if (it >= NST) gts_mbar_wait(&empty[s], ph ^ 1u);")
+    w("          if (it >= NST) gts_mbar_wait_sleep(&empty[s], ph ^ 1u);")
     w("          gts_mbar_arrive_expect_tx(&full[s], STB);")
     for f in sp.streamed:
-        w(f"          gts_tma_load_3d(smem + s * STB + {sp.offs_in_stage[f]}, &tm_{f}, &full[s], j0, i0, kb * {KB});")
+        w(f"          gts_tma_load_3d(smem + s * STB + {v.offs[f]}, &tm_{f}, &full[s], j0, i0, kb * {KB});")
     w("        }")
     w("      }")
     w("    }")
     w("  } else {")
-    w("    const uint32_t tl = tbase + ((uint32_t)(warp * 32) << 16);")
+    w(f"    const uint32_t tl = tbase + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)((warp >> 2) * {512 // v.w});")
+    w("    const int ct = threadIdx.x;")
     w("    int it = 0;")
-    # interval bounds
     gf = _interval_groups(msf)
     gb = _interval_groups(msb)
     for gi, (iv, _) in enumerate(gf):
@@ -247,105 +364,232 @@ def emit(kname: str, plan, kplan, sp: ThomasSpec, ctype: dict, dtypes: dict):
     for gi, (iv, _) in enumerate(gb):
         w(f"    const int b{gi}k0 = {_bound(iv.start)}, b{gi}k1 = {_bound(iv.end)};")
     w("    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {")
-    w(f"      const int j = (t % tiles_j) * {TJ} + lane, i = (t / tiles_j) * {TI} + warp;")
+    w(f"      const int j = (t % tiles_j) * {TJ} + lane, i = (t / tiles_j) * {rows} + warp;")
     w("      const bool valid = (i < p.ni) && (j < p.nj);")
     w("      const int ic = i < p.ni ? i : p.ni - 1, jc = j < p.nj ? j : p.nj - 1;")
     w("      (void)ic; (void)jc;")
-    # ---------------- forward
+    for f in impl.api_fields:
+        if any(f.name in writes(st.body) for st in msb.stages):
+            w(f"      {ctype[f.name]}* const colp_{f.name} = &GTS_AT(p.f_{f.name}, ic, jc, 0);")
     cf = _caches(msf, 1)
     wf = set()
     for st in msf.stages:
         wf |= writes(st.body)
-    tracked_f = sorted(wf)  # every forward-written temp lives in a register per level
+    tracked_f = sorted(wf)
+    cached_f = {f: d for f, d in cf.items()} | {f: 0 for f in tracked_f if f not in cf}
+
+    def store_hist(indent, tier):
+        if tier == "tmem":
+            for t in sp.cross:
+                col = f"(uint32_t)(k * {wl} + {sp.offsets[t]})"
+                if sp.words[t] == 2:
+                    w(f"{indent}gts_tmem_store_f64(tl + {col}, cur_{t});")
+                else:
+                    w(f"{indent}gts_tmem_store_f32(tl + {col}, (float)cur_{t});")
+        else:
+            w(f"{indent}{{ unsigned char* hl = hist + (size_t)(k - TL) * {hb * nct};")
+            for t in sp.cross:
+                w(f"{indent}  (({ctype[t]}*)(hl + {hoff[t]}))[ct] = ({ctype[t]})cur_{t};")
+            w(f"{indent}}}")
+
+    def forward_level(ctx, indent, group=None, tier=None):
+        """group: index of the statically known interval group (None =
+        dispatch per level); tier: "tmem" / "smem" (None = per-level)."""
+        for f in tracked_f:
+            w(f"{indent}double cur_{f} = GTS_NAN;")
+        groups = [gf[group]] if group is not None else gf
+        for gi, (iv, stages) in enumerate(groups):
+            if group is None:
+                kw = "if" if gi == 0 else "else if"
+                w(f"{indent}{kw} (k >= f{gi}k0 && k < f{gi}k1) {{")
+            else:
+                w(f"{indent}{{")
+            ctx.pool = DivPool(ctx.div_mode)
+            for st in stages:
+                _emit_stmt(st.body, ctx, ctype, api, indent + "  ", out)
+            w(f"{indent}}}")
+        if tier is None:
+            w(f"{indent}if (k < TL) {{")
+            store_hist(indent + "  ", "tmem")
+            w(f"{indent}}} else {{")
+            store_hist(indent + "  ", "smem")
+            w(f"{indent}}}")
+        else:
+            store_hist(indent, tier)
+        for f, depth in sorted(cf.items()):
+            for s_ in range(depth, 1, -1):
+                w(f"{indent}prev{s_}_{f} = prev{s_ - 1}_{f};")
+            w(f"{indent}prev1_{f} = cur_{f};")
+
     for f, depth in sorted(cf.items()):
-        for s in range(1, depth + 1):
-            w(f"      double prev{s}_{f} = GTS_NAN;")
+        for s_ in range(1, depth + 1):
+            w(f"      double prev{s_}_{f} = GTS_NAN;")
+    w("      bool bad_ = false;")
     w("      for (int kb = 0; kb < nkb; ++kb, ++it) {")
     w("        const int s = it % NST;")
     w("        const uint32_t ph = (uint32_t)(it / NST) & 1u;")
     w("        gts_mbar_wait(&full[s], ph);")
     w("        const unsigned char* sb = smem + s * STB;")
-    w(f"        #pragma unroll 2")
-    w(f"        for (int kk = 0; kk < {KB}; ++kk) {{")
-    w(f"          const int k = kb * {KB} + kk;")
-    w("          if (k < nk) {")
-    for f in tracked_f:
-        w(f"            double cur_{f} = GTS_NAN;")
-    ctx_f = _Ctx(dtypes, sp, "f", {f: d for f, d in cf.items()} | {f: 0 for f in tracked_f if f not in cf}, ctype)
-    for gi, (iv, stages) in enumerate(gf):
-        kw = "if" if gi == 0 else "else if"
-        w(f"            {kw} (k >= f{gi}k0 && k < f{gi}k1) {{")
-        for st in stages:
-            _emit_stmt(st.body, ctx_f, ctype, api, "              ", out)
-        w("            }")
-    # TMEM stores of the cross temporaries (converged, warp-uniform)
-    for t in sp.cross:
-        col = f"(uint32_t)(k * {sp.w_level} + {sp.offsets[t]})"
-        if sp.words[t] == 2:
-            w(f"            gts_tmem_store_f64(tl + {col}, cur_{t});")
-        else:
-            w(f"            gts_tmem_store_f32(tl + {col}, (float)cur_{t});")
-    for f, depth in sorted(cf.items()):
-        for s_ in range(depth, 1, -1):
-            w(f"            prev{s_}_{f} = prev{s_ - 1}_{f};")
-        w(f"            prev1_{f} = cur_{f};")
+    w(f"        const int kbase = kb * {KB};")
+    w(f"        const bool fullst = kbase + {KB} <= nk;")
+    ctx_f = _Ctx(dtypes, sp, "f", cached_f, ctype)
+    ctx_f.rows, ctx_f.kb, ctx_f.offs = rows, KB, v.offs
+    first = True
+    for tier, tcond in (("tmem", "kbase < TL"), ("smem", "kbase >= TL")):
+        for gi in range(len(gf)):
+            kw = "if" if first else "} else if"
+            first = False
+            w(f"        {kw} (fullst && {tcond} && kbase >= f{gi}k0 && kbase + {KB} <= f{gi}k1) {{")
+            w("          #pragma unroll")
+            w(f"          for (int kk = 0; kk < {KB}; ++kk) {{")
+            w("            const int k = kbase + kk;")
+            forward_level(ctx_f, "            ", gi, tier)
+            w("          }")
+    w("        } else {")
+    w("          #pragma unroll")
+    w(f"          for (int kk = 0; kk < {KB}; ++kk) {{")
+    w("            const int k = kbase + kk;")
+    w("            if (k < nk) {")
+    forward_level(ctx_f, "              ")
+    w("            }")
     w("          }")
     w("        }")
-    w("        gts_fence_proxy_async();")
     w("        __syncwarp();")
     w("        if (lane == 0) gts_mbar_arrive(&empty[s]);")
     w("      }")
+    w("      if (__any_sync(0xffffffffu, bad_)) {")
+    for f, depth in sorted(cf.items()):
+        for s_ in range(1, depth + 1):
+            w(f"        prev{s_}_{f} = GTS_NAN;")
+    w("        for (int k = 0; k < nk; ++k) {")
+    ctx_r = _Ctx(dtypes, sp, "f", cached_f, ctype)
+    ctx_r.ring, ctx_r.div_mode = False, "exact"
+    forward_level(ctx_r, "          ")
+    w("        }")
+    w("      }")
     w("      gts_tmem_wait_st();")
+    w("      __syncwarp();")
     # ---------------- backward
     cb = _caches(msb, -1)
     wb = set()
     for st in msb.stages:
         wb |= writes(st.body)
     for f, depth in sorted(cb.items()):
-        for s in range(1, depth + 1):
-            w(f"      double prev{s}_{f} = GTS_NAN;")
-    w("      for (int k = nk - 1; k >= 0; --k) {")
-    for t in sp.cross:
-        col = f"(uint32_t)(k * {sp.w_level} + {sp.offsets[t]})"
-        if sp.words[t] == 2:
-            w(f"        uint32_t lo_{t}, hi_{t};")
-            w(f"        gts_tmem_ld2(tl + {col}, lo_{t}, hi_{t});")
-        else:
-            w(f"        uint32_t lo_{t};")
-            w(f"        gts_tmem_ld1(tl + {col}, lo_{t});")
-    w("        gts_tmem_wait_ld();")
-    for t in sp.cross:
-        if sp.words[t] == 2:
-            w(f"        const double cur_{t} = __hiloint2double((int)hi_{t}, (int)lo_{t});")
-        else:
-            w(f"        const double cur_{t} = (double)__uint_as_float(lo_{t});")
-    for f in sorted(wb):
-        if f in api:
-            if f in cb:
-                # current value of a cached api output: memory unless written first
-                first_groups = gb
-                need = any(_need_load(stg, f) for _, stg in first_groups)
-                if need:
-                    w(f"        double cur_{f} = ((double)GTS_AT(p.f_{f}, ic, jc, k));")
-                else:
-                    w(f"        double cur_{f};")
-        else:
-            w(f"        double cur_{f} = GTS_NAN;")
+        for s_ in range(1, depth + 1):
+            w(f"      double prev{s_}_{f} = GTS_NAN;")
     cached_b = {t: 0 for t in sp.cross}
     cached_b.update({f: 0 for f in wb if f not in api})
     cached_b.update(cb)
     ctx_b = _Ctx(dtypes, sp, "b", cached_b, ctype)
-    for gi, (iv, stages) in enumerate(gb):
-        kw = "if" if gi == 0 else "else if"
-        w(f"        {kw} (k >= b{gi}k0 && k < b{gi}k1) {{")
-        for st in stages:
-            _emit_stmt(st.body, ctx_b, ctype, api, "          ", out)
-        w("        }")
-    for f, depth in sorted(cb.items()):
-        for s_ in range(depth, 1, -1):
-            w(f"        prev{s_}_{f} = prev{s_ - 1}_{f};")
-        w(f"        prev1_{f} = cur_{f};")
+    need_load = {f: any(_need_load(stg, f) for _, stg in gb) for f in wb if f in api and f in cb}
+
+    def backward_level(indent, hist_value, group=None):
+        for t in sp.cross:
+            w(f"{indent}const double cur_{t} = {hist_value(t)};")
+        for f in sorted(wb):
+            if f in api:
+                if f in cb:
+                    if need_load[f]:
+                        w(f"{indent}double cur_{f} = ((double)GTS_AT(p.f_{f}, ic, jc, k));")
+                    else:
+                        w(f"{indent}double cur_{f};")
+            else:
+                w(f"{indent}double cur_{f} = GTS_NAN;")
+        groups = [gb[group]] if group is not None else gb
+        for gi, (iv, stages) in enumerate(groups):
+            if group is None:
+                kw = "if" if gi == 0 else "else if"
+                w(f"{indent}{kw} (k >= b{gi}k0 && k < b{gi}k1) {{")
+            else:
+                w(f"{indent}{{")
+            ctx_b.pool = DivPool("branch")
+            for st in stages:
+                _emit_stmt(st.body, ctx_b, ctype, api, indent + "  ", out)
+            w(f"{indent}}}")
+        for f, depth in sorted(cb.items()):
+            for s_ in range(depth, 1, -1):
+                w(f"{indent}prev{s_}_{f} = prev{s_ - 1}_{f};")
+            w(f"{indent}prev1_{f} = cur_{f};")
+
+    if dbg == "fwdonly":
+        w("      if (nk > 100000) {")
+    # shared-memory tier: levels [TL, nk), visited first, in chunks of 4
+    def from_smem(t):
+        return f"(double)((const {ctype[t]}*)(hist + (size_t)(k - TL) * {hb * nct} + {hoff[t]}))[ct]"
+
+    w("      if (nk > TL) {")
+    w("        for (int c4 = (nk - 1 - TL) / 4; c4 >= 0; --c4) {")
+    w("          const int klo = TL + 4 * c4, khi = klo + 3;")
+    first = True
+    for gi in range(len(gb)):
+        kw = "if" if first else "} else if"
+        first = False
+        w(f"          {kw} (khi < nk && klo >= b{gi}k0 && khi < b{gi}k1) {{")
+        w("            #pragma unroll")
+        w("            for (int r = 3; r >= 0; --r) {")
+        w("              const int k = klo + r;")
+        backward_level("              ", from_smem, gi)
+        w("            }")
+    w("          } else {")
+    w("            #pragma unroll")
+    w("            for (int r = 3; r >= 0; --r) {")
+    w("              const int k = klo + r;")
+    w("              if (k < nk) {")
+    backward_level("                ", from_smem)
+    w("              }")
+    w("            }")
+    w("          }")
+    w("        }")
     w("      }")
+    # TMEM tier: batches of B levels (32 words per tcgen05.ld), double-buffered
+    if 32 % wl:
+        raise NotImplementedError("history words per level must divide 32")
+    B = 32 // wl
+
+    def from_regs(t):
+        base = f"r * {wl} + {sp.offsets[t]}"
+        if sp.words[t] == 2:
+            return f"__hiloint2double((int)hb_[{base} + 1], (int)hb_[{base}])"
+        return f"(double)__uint_as_float(hb_[{base}])"
+
+    w("      {")
+    w("        const int ktop = (nk < TL ? nk : TL) - 1;")
+    w("        if (ktop >= 0) {")
+    w("          uint32_t hb_[32], nb_[32];")
+    w(f"          int bi = ktop / {B};")
+    w("          gts_tmem_ld32(tl + (uint32_t)(bi * 32), nb_);")
+    w("          gts_tmem_wait_ld32(nb_);")
+    w("          for (; bi >= 0; --bi) {")
+    w("            #pragma unroll")
+    w("            for (int q = 0; q < 32; ++q) hb_[q] = nb_[q];")
+    w("            if (bi > 0) gts_tmem_ld32(tl + (uint32_t)((bi - 1) * 32), nb_);")
+    w(f"            const int klo = bi * {B}, khi = klo + {B - 1};")
+    first = True
+    for gi in range(len(gb)):
+        kw = "if" if first else "} else if"
+        first = False
+        w(f"            {kw} (khi <= ktop && klo >= b{gi}k0 && khi < b{gi}k1) {{")
+        w("              #pragma unroll")
+        w(f"              for (int r = {B - 1}; r >= 0; --r) {{")
+        w("                const int k = klo + r;")
+        backward_level("                ", from_regs, gi)
+        w("              }")
+    w("            } else {")
+    w("              #pragma unroll")
+    w(f"              for (int r = {B - 1}; r >= 0; --r) {{")
+    w("                const int k = klo + r;")
+    w("                if (k <= ktop) {")
+    backward_level("                  ", from_regs)
+    w("                }")
+    w("              }")
+    w("            }")
+    w("            gts_tmem_wait_ld32(nb_);")
+    w("          }")
+    w("        }")
+    w("      }")
+    if dbg == "fwdonly":
+        w("      }")
+    w("      __syncwarp();")
     w("    }")
     w("  }")
     w("  gts_tmem_fence_before_sync();")
@@ -353,32 +597,29 @@ def emit(kname: str, plan, kplan, sp: ThomasSpec, ctype: dict, dtypes: dict):
     w("  if (warp == 0) { gts_tmem_fence_after_sync(); gts_tmem_dealloc<512>(tbase); }")
     w("}")
 
-    # ---------------- host launch (falls back to the generic column kernel)
-    smem_bytes = sp.nstages * sp.stage_bytes + 2 * 8 * sp.nstages + 16
-    launch = ["  {", "    bool tmem_ok = (nk * %d <= 512);" % sp.w_level]
-    for f in sp.streamed:
-        e = 8 if dtypes[f] == ir.F64 else 4
-        launch.append(f"    CUtensorMap tm_{f};")
-        launch.append(
-            f"    tmem_ok = tmem_ok && gts_make_tmap_3d(&tm_{f}, (const void*)p.f_{f}.p, {e}, nj, ni, nk,"
-            f" p.f_{f}.si, p.f_{f}.sj, p.f_{f}.sk, {TJ}, {TI}, {KB});")
-    tm_args = ", ".join(f"tm_{f}" for f in sp.streamed)
-    launch += [
-        "    if (tmem_ok) {",
-        f"      const int tiles_j = (int)((nj + {TJ - 1}) / {TJ});",
-        f"      const int ntiles = tiles_j * (int)((ni + {TI - 1}) / {TI});",
-        "      int grid = gts_sm_count(); if (grid > ntiles) grid = ntiles;",
-        "      static bool attr_set = false;",
-        "      if (!attr_set) {",
-        f"        cudaFuncSetAttribute({kname}_tmem, cudaFuncAttributeMaxDynamicSharedMemorySize, {smem_bytes});",
-        "        attr_set = true;",
-        "      }",
-        f"      {kname}_tmem<<<grid, 160, {smem_bytes}, st>>>(p, {tm_args}, tiles_j, ntiles);",
-        "    } else {",
-        "      dim3 grid((unsigned)((nj + GTS_COL_TJ - 1) / GTS_COL_TJ),"
-        " (unsigned)((ni + (GTS_COL_THREADS / GTS_COL_TJ) - 1) / (GTS_COL_THREADS / GTS_COL_TJ)), 1);",
-        f"      {kname}<<<grid, GTS_COL_THREADS, 0, st>>>(p);",
-        "    }",
-        "  }",
-    ]
-    return out, launch
+    def call(vi):
+        tm_args = ", ".join(f"tm_{f}[{vi}]" for f in sp.streamed)
+        return [
+            f"const int tiles_j = (int)((nj + {TJ - 1}) / {TJ});",
+            f"const int ntiles = tiles_j * (int)((ni + {rows - 1}) / {rows});",
+            "int grid = gts_sm_count(); if (grid > ntiles) grid = ntiles;",
+            f"static bool attr_w{v.w} = false;",
+            f"if (!attr_w{v.w}) {{ cudaFuncSetAttribute({kn}, cudaFuncAttributeMaxDynamicSharedMemorySize, {v.smem_bytes}); attr_w{v.w} = true; }}",
+            f"{kn}<<<grid, {threads}, {v.smem_bytes}, st>>>(p, {tm_args}, tiles_j, ntiles);",
+        ]
+
+    return out, None, call
+
+
+class _PrefCtx(_Ctx):
+    """_Ctx with a per-sweep name prefix for the k-cache chains."""
+
+    def __init__(self, dtypes, sp, phase, cached, ctype, prefix):
+        super().__init__(dtypes, sp, phase, cached, ctype)
+        self.prefix = prefix
+
+    def read(self, name, off):
+        r = super().read(name, off)
+        if r.startswith("prev"):
+            return self.prefix + r[4:]
+        return r

@@ -45,6 +45,25 @@ __device__ __forceinline__ void gts_mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// Wait with back-off: for a producer warp that shares an SM sub-partition
+// with a consumer warp, so its polling does not steal issue slots.
+__device__ __forceinline__ bool gts_mbar_try(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, P1;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(gts_smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void gts_mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  while (!gts_mbar_try(bar, parity)) __nanosleep(200);
+}
+
 // Generic-proxy reads of a smem buffer must be ordered before the async
 // proxy (TMA) overwrites it.
 __device__ __forceinline__ void gts_fence_proxy_async() {
@@ -96,12 +115,10 @@ __device__ __forceinline__ void gts_tmem_fence_after_sync() {
 
 __device__ __forceinline__ void gts_tmem_st2(uint32_t taddr, uint32_t r0, uint32_t r1) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};" ::"r"(taddr), "r"(r0),
-               "r"(r1)
-               : "memory");
+               "r"(r1));
 }
 __device__ __forceinline__ void gts_tmem_st1(uint32_t taddr, uint32_t r0) {
-  asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(taddr), "r"(r0)
-               : "memory");
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(taddr), "r"(r0));
 }
 __device__ __forceinline__ void gts_tmem_wait_st() {
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
@@ -110,17 +127,43 @@ __device__ __forceinline__ void gts_tmem_wait_st() {
 __device__ __forceinline__ void gts_tmem_ld2(uint32_t taddr, uint32_t& r0, uint32_t& r1) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];"
                : "=r"(r0), "=r"(r1)
-               : "r"(taddr)
-               : "memory");
+               : "r"(taddr));
 }
 __device__ __forceinline__ void gts_tmem_ld1(uint32_t taddr, uint32_t& r0) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];"
                : "=r"(r0)
-               : "r"(taddr)
-               : "memory");
+               : "r"(taddr));
 }
 __device__ __forceinline__ void gts_tmem_wait_ld() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// wait::ld tied to the destination registers, so no use of them can be
+// scheduled before the wait completes.
+__device__ __forceinline__ void gts_tmem_wait_ld_r2(uint32_t& r0, uint32_t& r1) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(r0), "+r"(r1)::"memory");
+}
+__device__ __forceinline__ void gts_tmem_wait_ld_r4(uint32_t& r0, uint32_t& r1, uint32_t& r2,
+                                                    uint32_t& r3) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(r0), "+r"(r1), "+r"(r2), "+r"(r3)::"memory");
+}
+__device__ __forceinline__ void gts_tmem_ld4(uint32_t taddr, uint32_t& r0, uint32_t& r1,
+                                             uint32_t& r2, uint32_t& r3) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(taddr));
+}
+
+
+// 32 consecutive TMEM columns of this thread's lane in one instruction
+// (e.g. 8 levels x 4 words of a Thomas history), and a wait tied to them.
+__device__ __forceinline__ void gts_tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+               : "r"(taddr));
+}
+__device__ __forceinline__ void gts_tmem_wait_ld32(uint32_t (&r)[32]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]), "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15]), "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]), "+r"(r[22]), "+r"(r[23]), "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]), "+r"(r[29]), "+r"(r[30]), "+r"(r[31])::"memory");
 }
 
 __device__ __forceinline__ void gts_tmem_store_f64(uint32_t taddr, double v) {

@@ -1,0 +1,51 @@
+"""Summarise an ncu report: key metrics + top stall reasons (run here, no GPU).
+
+    python profiles/ncu_summary.py gpurun_out/x.ncu-rep [--source]
+"""
+import csv
+import io
+import subprocess
+import sys
+
+KEYS = [
+    "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+    "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "lts__t_bytes.sum",
+    "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+    "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
+    "launch__grid_size", "launch__block_size", "launch__shared_mem_per_block_dynamic",
+    "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
+    "smsp__inst_executed.sum", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
+    "smsp__cycles_active.avg", "sm__cycles_elapsed.avg",
+]
+
+
+def raw(path):
+    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    return rows[0], rows[1], rows[2:]
+
+
+def main():
+    path = sys.argv[1]
+    hdr, units, data = raw(path)
+    for r in data:
+        name = r[hdr.index("Kernel Name")] if "Kernel Name" in hdr else "?"
+        print(f"== {name[:90]}")
+        for k in KEYS:
+            if k in hdr:
+                print(f"  {k:70s} {r[hdr.index(k)]:>16s} {units[hdr.index(k)]}")
+        stalls = []
+        for i, h in enumerate(hdr):
+            if h.startswith("smsp__average_warp_latency_issue_stalled_") or (
+                    h.startswith("smsp__pcsamp_warps_issue_stalled_") and not h.endswith("_not_issued")):
+                try:
+                    stalls.append((float(r[i]), h))
+                except ValueError:
+                    pass
+        for v, h in sorted(stalls, reverse=True)[:10]:
+            print(f"  stall {h:70s} {v:12.1f}")
+
+
+if __name__ == "__main__":
+    main()
