@@ -369,14 +369,22 @@ def generate_source(plan: Plan, fp, options: Optional[dict] = None) -> str:
     w(f"// plan: {' '.join(plan.describe())}")
     w('#include "gts_common.cuh"')
     w('#include "gts_sm100.cuh"')
-    if any(k.kind == "pfused" for k in plan.kernels):
-        w('#include "gts_parallel.cuh"')
     w("")
+    # temporaries with device storage: the plan's arena temporaries, plus the
+    # register-only temporaries of fused launches (used only by their
+    # per-stage fallback when the fields are not TMA-compatible)
+    local_of = {}
+    for kidx, k in enumerate(plan.kernels):
+        if k.kind == "pfused":
+            for t in k.local_temps:
+                local_of[t] = kidx
+    arena_temps = list(plan.global_temps) + sorted(local_of)
     w("struct GtsParams {")
     w("  int ni, nj, nk;")
     for f in impl.api_fields:
         w(f"  GtsField<{ctype[f.name]}> f_{f.name};")
-    for t in plan.global_temps:
+        w(f"  int tsh_{f.name}_i, tsh_{f.name}_j, tsh_{f.name}_k;")
+    for t in arena_temps:
         w(f"  GtsField<{ctype[t]}> f_{t};")
     for s in impl.api_scalars:
         w(f"  double sc_{s.name};")
@@ -384,8 +392,48 @@ def generate_source(plan: Plan, fp, options: Optional[dict] = None) -> str:
     w("")
 
     launches: list = []  # host-side launch code lines
+    prelude: list = []  # host-side lines before the arena is sized
+    fused_ok: dict = {}  # kernel index -> C flag name
+
+    def pstage_launch(kname, st):
+        e = st.compute_extent
+        return [
+            "  {",
+            f"    const int k0 = {_bound(st.interval.start)}, k1 = {_bound(st.interval.end)};",
+            f"    const int i0 = {e.lo[0]}, i1 = (int)ni + {e.hi[0]};",
+            f"    const int j0 = {e.lo[1]}, j1 = (int)nj + {e.hi[1]};",
+            "    if (k0 < k1 && i0 < i1 && j0 < j1) {",
+            "      for (int kb = k0; kb < k1; kb += 65535) {",
+            "        dim3 grid((unsigned)((j1 - j0 + 31) / 32), (unsigned)((i1 - i0 + 7) / 8),"
+            " (unsigned)((k1 - kb) < 65535 ? (k1 - kb) : 65535));",
+            f"        {kname}<<<grid, 256, 0, st>>>(p, i0, i1, j0, j1, kb);",
+            "      }",
+            "    }",
+            "  }",
+        ]
+
     for kidx, k in enumerate(plan.kernels):
         kname = f"gts_k{kidx}_{k.kind}"
+        if k.kind == "pfused":
+            res = codegen_parallel.emit(kname, plan, k, ctype, dtypes) if opts.get("tma", True) else None
+            fb = []
+            for r in k.stages:
+                nm = f"{kname}_s{r.idx}"
+                out.extend(_point_kernel(nm, r.stage, ctype, dtypes))
+                fb += pstage_launch(nm, r.stage)
+            if res is None:
+                launches += fb
+                for t in k.local_temps:
+                    local_of[t] = -1  # always needs its arena slot
+            else:
+                code, pre, launch = res
+                out.extend(code)
+                flag = f"fz_ok_{kidx}"
+                fused_ok[kidx] = flag
+                prelude += pre
+                launches += [f"  if ({flag}) {{"] + launch + ["  } else {"] + fb + ["  }"]
+            w("")
+            continue
         if k.kind == "pstage":
             st = k.stages[0].stage
             out.extend(_point_kernel(kname, st, ctype, dtypes))
@@ -447,10 +495,6 @@ def generate_source(plan: Plan, fp, options: Optional[dict] = None) -> str:
                 f"    {kname}<<<grid, GTS_COL_THREADS, 0, st>>>(p);",
                 "  }",
             ]
-        elif k.kind == "pfused":
-            code, launch = codegen_parallel.emit(kname, plan, k, ctype, dtypes)
-            out.extend(code)
-            launches += launch
         else:
             raise ValueError(k.kind)
         w("")
@@ -478,24 +522,34 @@ def generate_source(plan: Plan, fp, options: Optional[dict] = None) -> str:
         w(f"  p.f_{n} = gts_field(f_{n}, s_{n}_i, s_{n}_j, s_{n}_k, o_{n}_i, o_{n}_j, o_{n}_k);")
     for s in impl.api_scalars:
         w(f"  p.sc_{s.name} = sc_{s.name};")
-    if plan.global_temps:
+    out.extend(prelude)
+    if arena_temps:
         w("  // device arena for temporaries: shape = domain + extent (common.py:58-69),")
         w("  // k outermost, j contiguous, rows padded to 128 B; persistent across calls")
         w("  size_t arena_bytes = 0;")
-        for t in plan.global_temps:
+        for t in arena_temps:
             e = temps[t].extent
+            kk = local_of.get(t)
+            need = f"!{fused_ok[kk]}" if kk is not None and kk in fused_ok else "true"
+            w(f"  const bool need_{t} = {need};")
             w(f"  const int64_t td_{t}_i = ni + {e.hi[0] - e.lo[0]}, td_{t}_j = nj + {e.hi[1] - e.lo[1]};")
             w(f"  const int64_t tp_{t} = gts_pad_row(td_{t}_j, sizeof({ctype[t]}));")
             w(f"  const size_t toff_{t} = arena_bytes;")
-            w(f"  arena_bytes += gts_round_up((size_t)(td_{t}_i * tp_{t} * nk) * sizeof({ctype[t]}), 256);")
-        w("  char* arena = (char*)gts_arena(arena_bytes, st);")
-        w(f"  if (!arena) return {GTS_ERR_ALLOC};")
-        for t in plan.global_temps:
+            w(f"  if (need_{t}) arena_bytes += gts_round_up((size_t)(td_{t}_i * tp_{t} * nk) * sizeof({ctype[t]}), 256);")
+        w("  char* arena = arena_bytes ? (char*)gts_arena(arena_bytes, st) : nullptr;")
+        w(f"  if (arena_bytes && !arena) return {GTS_ERR_ALLOC};")
+        for t in arena_temps:
             e = temps[t].extent
-            w(f"  p.f_{t} = gts_field(({ctype[t]}*)(arena + toff_{t}), tp_{t}, 1, td_{t}_i * tp_{t},"
+            w(f"  if (need_{t}) p.f_{t} = gts_field(({ctype[t]}*)(arena + toff_{t}), tp_{t}, 1, td_{t}_i * tp_{t},"
               f" {-e.lo[0]}, {-e.lo[1]}, 0);")
-        for t in plan.nan_fill_temps:
-            w(f"  gts_fill_nan(arena + toff_{t}, (size_t)(td_{t}_i * tp_{t} * nk), sizeof({ctype[t]}), st);")
+        nanf = set(plan.nan_fill_temps)
+        for k in plan.kernels:
+            for t in k.local_temps:
+                for r in k.stages:
+                    if t in writes(r.stage.body) and t not in always_writes(r.stage.body):
+                        nanf.add(t)
+        for t in sorted(nanf):
+            w(f"  if (need_{t}) gts_fill_nan(arena + toff_{t}, (size_t)(td_{t}_i * tp_{t} * nk), sizeof({ctype[t]}), st);")
     out.extend(launches)
     w("  return (int)cudaGetLastError();")
     w("}")

@@ -1,5 +1,397 @@
-"""Fused PARALLEL streaming-tile template instantiation (placeholder)."""
+"""Fused PARALLEL template: one streaming tile kernel for a group of stages.
+
+Instantiates hdiff-class PARALLEL multistages (stencilforge
+``kernels/hdiff.gts:3-15``: Laplacian -> limited fluxes -> update) as one
+persistent sm_100a kernel in which every api field crosses HBM once:
+
+* tile = one k-plane x (NW*RI rows) x (32*VJ columns); 4 warps per CTA,
+  several CTAs per SM, a static round-robin over tiles;
+* each input field's tile plus its halo (the field extent from
+  ``analysis.compute_extents``, ``analysis.py:451-496``) is brought into
+  shared memory by ONE TMA box load (``cp.async.bulk.tensor.3d``) into a
+  double buffer, the next tile's box in flight while this one computes;
+* each warp streams its RI-row strip along i; lane l owns VJ consecutive
+  j columns.  Every stage is computed at its leading row (row + its i-extent
+  ``hi``) over its column span (VJ columns + its j-extent), so temporaries
+  live in small rolling register windows -- recomputed on the horizontal
+  halo exactly as the extent analysis prescribes, never stored;
+* outputs are written straight from registers.
+
+Semantics: within a fused group every temporary has a single writer and
+every read of a group-written api field is at the reader's own point
+(lowering._fuse_parallel), so executing all stages per point in program
+order equals the reference's whole-slab-per-stage order (``vec.py:160-162``).
+Reads the streaming scheme does not cover (vertical offsets, arena
+temporaries) go to global memory directly.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+from ._host import ir
+from .codegen import DivPool, _bound, c_float, emit_expr  # noqa: F401
+from .lowering import always_writes, reads, writes
+
+NW = 4  # warps per CTA
+RI = 8  # rows per warp strip
+VJ = 4  # columns per lane
+TJ = 32 * VJ  # columns per tile
+TI = NW * RI  # rows per tile
+SMEM_BUDGET = 110 * 1024  # per CTA (2 CTAs / SM)
 
 
-def emit(kname, plan, kplan, ctype, dtypes):
-    raise NotImplementedError("pfused kernels are not implemented yet")
+@dataclass
+class Win:
+    name: str
+    kind: str  # "temp" (register window fed by a stage) | "stream" (TMA tile) | "own" (api written, own point)
+    rlo: int = 0  # rows relative to the step row
+    rhi: int = 0
+    clo: int = 0  # columns relative to the lane's first column
+    chi: int = 0
+    producer: int = -1
+    # stream geometry
+    box_cols: int = 0
+    box_rows: int = 0
+    cshift: int = 0  # the map base column (lo_j - cshift) is 16-B aligned
+    bstart: int = 0  # box start column relative to the tile's first column
+    smem_off: int = 0
+    esize: int = 8
+
+
+@dataclass
+class Geo:
+    stages: list
+    ext: list  # per stage (li, hi, lj, hj)
+    wins: dict = field(default_factory=dict)
+    min_step: int = 0
+    buf_bytes: int = 0  # one buffer (all streamed fields)
+
+
+def _cn(col: int) -> str:
+    return f"m{-col}" if col < 0 else str(col)
+
+
+def _stage_ext(st):
+    e = st.compute_extent
+    return (e.lo[0], e.hi[0], e.lo[1], e.hi[1])
+
+
+def analyse(plan, kplan, dtypes: dict) -> Geo:
+    impl = plan.impl
+    api = {f.name for f in impl.api_fields}
+    stages = [r.stage for r in kplan.stages]
+    ext = [_stage_ext(st) for st in stages]
+    geo = Geo(stages, ext)
+    local = set(kplan.local_temps)
+    written = set()
+    for si, st in enumerate(stages):
+        li, hi, lj, hj = ext[si]
+        for acc in reads(st.body):
+            di, dj, dk = acc.offset
+            name = acc.field
+            if dk != 0:
+                continue  # vertical reads of pure inputs: direct loads
+            if name in local:
+                kind = "temp"
+            elif name in written and name in api:
+                kind = "own"
+            elif name in api and all(name not in writes(s2.body) for s2 in stages):
+                kind = "stream"
+            else:
+                continue  # arena temporaries / other: direct loads
+            rows = (hi + di, hi + di)
+            cols = (lj + dj, VJ - 1 + hj + dj)
+            wv = geo.wins.get(name)
+            if wv is None:
+                wv = geo.wins[name] = Win(name, kind, rows[0], rows[1], cols[0], cols[1])
+            else:
+                wv.rlo, wv.rhi = min(wv.rlo, rows[0]), max(wv.rhi, rows[1])
+                wv.clo, wv.chi = min(wv.clo, cols[0]), max(wv.chi, cols[1])
+        for f in writes(st.body):
+            written.add(f)
+            if f in geo.wins and geo.wins[f].kind == "temp" and geo.wins[f].producer < 0:
+                geo.wins[f].producer = si
+    for si, st in enumerate(stages):
+        for f in writes(st.body):
+            if f in local:
+                wv = geo.wins.get(f)
+                if wv is None:
+                    geo.wins[f] = Win(f, "temp", 0, 0, 0, 0, producer=si)
+                else:
+                    wv.producer = si
+    for name, wv in geo.wins.items():
+        if wv.kind == "temp":
+            li, hi, lj, hj = ext[wv.producer]
+            # the window keeps rows [rlo, hi] of the producer's output
+            wv.rhi = hi
+            wv.rlo = min(wv.rlo, hi)
+            wv.clo = min(wv.clo, lj)
+            wv.chi = max(wv.chi, VJ - 1 + hj)
+    geo.min_step = min(li - hi for (li, hi, lj, hj) in ext)
+    off = 0
+    for name, wv in sorted(geo.wins.items()):
+        if wv.kind != "stream":
+            continue
+        e = 8 if dtypes[name] == ir.F64 else 4
+        wv.esize = e
+        align = 16 // e
+        lo_j = plan.impl.field_extent(name).lo[1]
+        wv.cshift = lo_j % align  # map base column lo_j - cshift is 16-B aligned
+        mb = lo_j - wv.cshift
+        # TMA boxes must start on a 16-B boundary of the inner dimension:
+        # round the box start down onto the map's 16-B grid
+        wv.bstart = mb + ((wv.clo - mb) // align) * align
+        ncols = (TJ - VJ + wv.chi) - wv.bstart + 1
+        ncols = -(-ncols // align) * align
+        wv.box_cols = ncols
+        wv.box_rows = TI + (wv.rhi - wv.rlo) - geo.min_step
+        wv.smem_off = off
+        off += wv.box_cols * wv.box_rows * e
+        off = -(-off // 128) * 128
+    geo.buf_bytes = off
+    return geo
+
+
+def eligible(plan, kplan, dtypes: dict):
+    geo = analyse(plan, kplan, dtypes)
+    for st in geo.stages:
+        for acc in reads(st.body):
+            if acc.offset[2] != 0 or acc.field not in geo.wins:
+                return None  # vertical offsets / arena reads: per-stage kernels
+    if not any(w.kind == "stream" for w in geo.wins.values()):
+        return None
+    for w in geo.wins.values():
+        if w.kind == "stream" and (w.box_cols > 256 or w.box_rows > 256):
+            return None
+    if 2 * geo.buf_bytes + 64 > SMEM_BUDGET:
+        return None
+    return geo
+
+
+class _Ctx:
+    """Read spelling inside one (row-offset, column) point of a stage."""
+
+    pool = None
+
+    def __init__(self, geo: Geo, ctype: dict, stage_hi: int, col: int):
+        self.geo, self.ctype, self.hi, self.col = geo, ctype, stage_hi, col
+
+    def read(self, name, off):
+        di, dj, dk = off
+        wv = self.geo.wins.get(name)
+        if wv is not None and dk == 0:
+            row = self.hi + di - wv.rlo
+            c = self.col + dj - wv.clo
+            if wv.kind == "stream":
+                return f"w_{name}[{row}][{c}]"
+            return f"w_{name}[{row}][{c}]"
+        # direct global load at the point (row r + hi + di, column j + col + dj)
+        return (f"((double)GTS_AT(p.f_{name}, (r + {self.hi + di}), "
+                f"(jl + {self.col + dj}), (kk + {dk})))")
+
+
+def _emit_point(stmt, ctx: _Ctx, ctype, api: set, out: list, indent: str, local: set,
+                geo: Geo) -> None:
+    """Stage body at one (row, column) point; writes go to the window slot of
+    a temp / own-point api field, api stores are guarded by validity."""
+    pool = ctx.pool
+    if isinstance(stmt, ir.Assign):
+        name = stmt.target.field
+        value = emit_expr(stmt.value, ctx)
+        pool.flush(indent, out)
+        out.append(f"{indent}{{ const double v_ = {value};")
+        wv = geo.wins.get(name)
+        if wv is not None and wv.kind in ("temp", "own"):
+            row = ctx.hi - wv.rlo
+            c = ctx.col - wv.clo
+            out.append(f"{indent}  w_{name}[{row}][{c}] = (double)({ctype[name]})(v_);")
+        if name in api:
+            out.append(f"{indent}  if (ok_{_cn(ctx.col)}) GTS_AT(p.f_{name}, r, (jl + {ctx.col}), kk) = ({ctype[name]})(v_);")
+        elif name in ctx.arena:
+            # arena copy for later launches: every point of the stage's extent
+            li, hi, lj, hj = ctx.stage_ext
+            out.append(f"{indent}  if ((r + {hi}) < ni + {hi} && (jl + {ctx.col}) >= {lj} && (jl + {ctx.col}) < nj + {hj})"
+                       f" GTS_AT(p.f_{name}, (r + {hi}), (jl + {ctx.col}), kk) = ({ctype[name]})(v_);")
+        out.append(f"{indent}}}")
+        pool.invalidate(name)
+        return
+    if isinstance(stmt, ir.If):
+        cond = emit_expr(stmt.cond, ctx)
+        pool.flush(indent, out)
+        out.append(f"{indent}if ({cond}) {{")
+        pool.depth += 1
+        for s in stmt.then_body:
+            _emit_point(s, ctx, ctype, api, out, indent + "  ", local, geo)
+        if stmt.else_body:
+            out.append(f"{indent}}} else {{")
+            for s in stmt.else_body:
+                _emit_point(s, ctx, ctype, api, out, indent + "  ", local, geo)
+        pool.depth -= 1
+        out.append(f"{indent}}}")
+        return
+    raise TypeError(type(stmt).__name__)
+
+
+def emit(kname: str, plan, kplan, ctype: dict, dtypes: dict):
+    geo = eligible(plan, kplan, dtypes)
+    if geo is None:
+        return None
+    impl = plan.impl
+    api = {f.name for f in impl.api_fields}
+    local = set(kplan.local_temps)
+    streams = [w for _, w in sorted(geo.wins.items()) if w.kind == "stream"]
+    regw = [w for _, w in sorted(geo.wins.items()) if w.kind != "stream"]
+    nst = len(streams)
+    out: list = []
+    w = out.append
+    tm = ", ".join(f"const __grid_constant__ CUtensorMap tm_{s.name}" for s in streams)
+    smem = 2 * geo.buf_bytes
+    bar_off = smem
+    w(f"// fused PARALLEL tile kernel: {TI}x{TJ} tile per k-plane, {NW} warps x {RI} rows, "
+      f"{VJ} columns/lane; streamed {[s.name for s in streams]}, register windows "
+      f"{[(x.name, x.rlo, x.rhi, x.clo, x.chi) for x in regw]}")
+    w(f"__global__ void __launch_bounds__({32 * NW}) {kname}(const __grid_constant__ GtsParams p, {tm}, "
+      "int k0, int nkr, int tiles_i, int tiles_j, int ntiles) {")
+    w("  extern __shared__ __align__(1024) unsigned char smem[];")
+    w(f"  uint64_t* full = (uint64_t*)(smem + {bar_off});")
+    w("  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;")
+    w("  if (threadIdx.x == 0) { gts_mbar_init(&full[0], 1); gts_mbar_init(&full[1], 1); gts_fence_mbar_init(); }")
+    w("  __syncthreads();")
+    w(f"  const int ni = p.ni, nj = p.nj;")
+
+    def issue(tvar, buf):
+        w(f"    {{ const int tt = {tvar};")
+        w("      const int kk_ = k0 + tt / (tiles_i * tiles_j);")
+        w("      const int rem_ = tt % (tiles_i * tiles_j);")
+        w(f"      const int i0_ = (rem_ / tiles_j) * {TI}, j0_ = (rem_ % tiles_j) * {TJ};")
+        w(f"      gts_mbar_arrive_expect_tx(&full[{buf}], {sum(x.box_cols * x.box_rows * x.esize for x in streams)}u);")
+        for s in streams:
+            w(f"      gts_tma_load_3d(smem + {buf} * {geo.buf_bytes} + {s.smem_off}, &tm_{s.name}, &full[{buf}], "
+              f"j0_ + ({s.bstart}) + jsh_{s.name}, i0_ + ({geo.min_step + s.rlo}) + ish_{s.name}, kk_ + ksh_{s.name});")
+        w("    }")
+
+    # the tensor maps start at the field's extent corner; shifts passed as constants
+    for s in streams:
+        w(f"  const int jsh_{s.name} = p.tsh_{s.name}_j, ish_{s.name} = p.tsh_{s.name}_i, ksh_{s.name} = p.tsh_{s.name}_k;")
+    w("  int it = 0;")
+    w("  if (threadIdx.x == 0 && (int)blockIdx.x < ntiles) {")
+    issue("(int)blockIdx.x", 0)
+    w("  }")
+    w("  for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {")
+    w("    const int buf = it & 1;")
+    w("    const uint32_t ph = (uint32_t)(it >> 1) & 1u;")
+    w("    // prefetch the next tile into the other buffer (freed at the end of the previous tile)")
+    w("    if (threadIdx.x == 0 && t + (int)gridDim.x < ntiles) {")
+    w("      gts_fence_proxy_async();")
+    w("      if (buf == 0) {")
+    issue("t + (int)gridDim.x", 1)
+    w("      } else {")
+    issue("t + (int)gridDim.x", 0)
+    w("      }")
+    w("    }")
+    w("    gts_mbar_wait(&full[buf], ph);")
+    w("    const unsigned char* sb = smem + buf * " + str(geo.buf_bytes) + ";")
+    w("    const int kk = k0 + t / (tiles_i * tiles_j);")
+    w("    const int rem = t % (tiles_i * tiles_j);")
+    w(f"    const int i0 = (rem / tiles_j) * {TI}, j0 = (rem % tiles_j) * {TJ};")
+    w(f"    const int jl = j0 + lane * {VJ};")
+    w(f"    const int ra = i0 + warp * {RI};")
+    # per-column store validity
+    for c in range(VJ):
+        w(f"    const bool okc_{c} = (jl + {c}) < nj;")
+    # register windows
+    for x in regw:
+        w(f"    double w_{x.name}[{x.rhi - x.rlo + 1}][{x.chi - x.clo + 1}];")
+    # stream windows are read from smem directly: define accessor macros
+    for s in streams:
+        row_base = geo.min_step + s.rlo  # smem row 0 <-> absolute row i0 + row_base
+        w(f"    const {ctype[s.name]}* const sp_{s.name} = (const {ctype[s.name]}*)(sb + {s.smem_off});")
+        w(f"    double w_{s.name}[{s.rhi - s.rlo + 1}][{s.chi - s.clo + 1}];")
+    steps_lo = geo.min_step
+    nsteps = RI - steps_lo  # steps r = ra + min_step .. ra + RI - 1
+
+    def load_stream_row(s, rowidx, rel_row):
+        # absolute row = r + rel_row; smem row = (r + rel_row) - (i0 + min_step + rlo)
+        for c in range(s.chi - s.clo + 1):
+            lane_col = f"(lane * {VJ} + {s.clo - s.bstart + c})"
+            w(f"      w_{s.name}[{rowidx}][{c}] = (double)sp_{s.name}[(size_t)((r + {rel_row}) - (i0 + {geo.min_step + s.rlo})) * {s.box_cols} + {lane_col}];")
+
+    # fully unrolled steps (prologue + main)
+    for step in range(nsteps):
+        rel = steps_lo + step  # r = ra + rel
+        w(f"    {{ // step r = ra + {rel}")
+        w(f"      const int r = ra + {rel};")
+        # shift windows (rows move down by one)
+        if step > 0:
+            for x in regw + streams:
+                depth = x.rhi - x.rlo + 1
+                for d in range(depth - 1):
+                    w(f"      #pragma unroll")
+                    w(f"      for (int c = 0; c < {x.chi - x.clo + 1}; ++c) w_{x.name}[{d}][c] = w_{x.name}[{d + 1}][c];")
+        # load stream rows: at the first step the whole window, later the top row
+        for s in streams:
+            if step == 0:
+                for d in range(s.rhi - s.rlo + 1):
+                    load_stream_row(s, d, s.rlo + d)
+            else:
+                load_stream_row(s, s.rhi - s.rlo, s.rhi)
+        # stages in program order; stage s computes row r + hi_s if that row is needed
+        for si, st in enumerate(geo.stages):
+            li, hi, lj, hj = geo.ext[si]
+            # needed rows for stage s: [ra + li, ra + RI - 1 + hi]; row computed = r + hi
+            if rel + hi < li:
+                continue  # prologue: this stage has nothing to produce yet
+            w(f"      {{ // stage {si} at row r + {hi}")
+            for col in range(lj, VJ + hj):
+                ctx = _Ctx(geo, ctype, hi, col)
+                ctx.pool = DivPool("branch")
+                ctx.arena = set(plan.global_temps)
+                ctx.stage_ext = geo.ext[si]
+                w(f"        {{ const bool ok_{_cn(col)} = {'okc_' + str(col) if 0 <= col < VJ else 'false'} && (r + {hi}) < ni && {hi} == 0;")
+                for f in sorted(writes(st.body) - always_writes(st.body)):
+                    wv = geo.wins.get(f)
+                    if wv is not None and wv.kind in ("temp", "own"):
+                        # a conditionally written temporary reads as NaN where
+                        # unwritten, like the reference's NaN-initialised ones
+                        w(f"          w_{f}[{hi - wv.rlo}][{col - wv.clo}] = GTS_NAN;")
+                _emit_point(st.body, ctx, ctype, api, out, "          ", local, geo)
+                w("        }")
+            w("      }")
+        w("    }")
+    w("    __syncthreads();  // both buffers' readers done before the next prefetch reuses this one")
+    w("  }")
+    w("}")
+
+    smem_bytes = smem + 16
+    flag = f"fz_ok_{kname.split('_')[1][1:]}"
+    pre = [f"  // TMA maps of {kname}: each covers the field's required region (its extent)"]
+    for s in streams:
+        pre.append(f"  CUtensorMap tm_{kname}_{s.name};")
+    pre.append(f"  bool {flag} = true;")
+    for s in streams:
+        e = s.esize
+        fe = plan.impl.field_extent(s.name)
+        pre += [
+            f"  p.tsh_{s.name}_i = -({fe.lo[0]}); p.tsh_{s.name}_j = -({fe.lo[1]} - {s.cshift}); p.tsh_{s.name}_k = 0;",
+            f"  {flag} = {flag} && gts_make_tmap_3d(&tm_{kname}_{s.name}, (const void*)&GTS_AT(p.f_{s.name}, {fe.lo[0]}, {fe.lo[1]} - {s.cshift}, 0), {e},"
+            f" nj + {fe.hi[1] - fe.lo[1]} + {s.cshift}, ni + {fe.hi[0] - fe.lo[0]}, nk, p.f_{s.name}.si, p.f_{s.name}.sj, p.f_{s.name}.sk,"
+            f" {s.box_cols}, {s.box_rows}, 1);",
+        ]
+    tm_args = ", ".join(f"tm_{kname}_{s.name}" for s in streams)
+    launch = [
+        "    {",
+        f"      const int k0 = {_bound(kplan.interval.start)}, k1 = {_bound(kplan.interval.end)};",
+        f"      const int tiles_i = (int)((ni + {TI - 1}) / {TI}), tiles_j = (int)((nj + {TJ - 1}) / {TJ});",
+        "      const int nkr = k1 - k0;",
+        "      if (nkr > 0) {",
+        "        const int ntiles = tiles_i * tiles_j * nkr;",
+        "        int grid = 2 * gts_sm_count(); if (grid > ntiles) grid = ntiles;",
+        "        static bool attr = false;",
+        f"        if (!attr) {{ cudaFuncSetAttribute({kname}, cudaFuncAttributeMaxDynamicSharedMemorySize, {smem_bytes}); attr = true; }}",
+        f"        {kname}<<<grid, {32 * NW}, {smem_bytes}, st>>>(p, {tm_args}, k0, nkr, tiles_i, tiles_j, ntiles);",
+        "      }",
+        "    }",
+    ]
+    return out, pre, launch
+

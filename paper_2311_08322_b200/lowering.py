@@ -198,7 +198,7 @@ def _fuse_parallel(stages: list, temp_names: set, fuse: bool) -> list:
 
 def build_plan(impl, options: Optional[dict] = None) -> Plan:
     opts = options or {}
-    fuse = bool(opts.get("fuse_parallel", False))
+    fuse = bool(opts.get("fuse_parallel", True))
     column = bool(opts.get("column", True))
     temp_names = {t.name for t in impl.temporaries}
     mss = list(impl.multistages)
