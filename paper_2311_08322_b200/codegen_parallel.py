@@ -38,7 +38,8 @@ RI = 8  # rows per warp strip
 VJ = 4  # columns per lane
 TJ = 32 * VJ  # columns per tile
 TI = NW * RI  # rows per tile
-SMEM_BUDGET = 110 * 1024  # per CTA (2 CTAs / SM)
+SMEM_BUDGET = 110 * 1024  # per CTA
+NBUF = 1  # tile buffers per CTA: latency is hidden across the CTAs of an SM
 
 
 @dataclass
@@ -66,6 +67,16 @@ class Geo:
     wins: dict = field(default_factory=dict)
     min_step: int = 0
     buf_bytes: int = 0  # one buffer (all streamed fields)
+    rot: int = 0  # emission-time step counter (window rotation)
+    buffered: set = field(default_factory=set)  # api outputs stored per row at step end
+
+
+def _phys(geo, wv, d: int) -> int:
+    """Rotating register windows: logical row d of a window lives in physical
+    row (d + step) mod depth, so sliding the window costs no register moves
+    in the fully unrolled step sequence."""
+    depth = wv.rhi - wv.rlo + 1
+    return (d + geo.rot) % depth
 
 
 def _cn(col: int) -> str:
@@ -129,6 +140,13 @@ def analyse(plan, kplan, dtypes: dict) -> Geo:
             wv.clo = min(wv.clo, lj)
             wv.chi = max(wv.chi, VJ - 1 + hj)
     geo.min_step = min(li - hi for (li, hi, lj, hj) in ext)
+    writers: dict = {}
+    for si, st in enumerate(stages):
+        for f in writes(st.body):
+            writers.setdefault(f, []).append(si)
+    for f, ws in writers.items():
+        if f in api and len(ws) == 1 and ext[ws[0]] == (0, 0, 0, 0) and f in always_writes(stages[ws[0]].body):
+            geo.buffered.add(f)
     off = 0
     for name, wv in sorted(geo.wins.items()):
         if wv.kind != "stream":
@@ -164,7 +182,7 @@ def eligible(plan, kplan, dtypes: dict):
     for w in geo.wins.values():
         if w.kind == "stream" and (w.box_cols > 256 or w.box_rows > 256):
             return None
-    if 2 * geo.buf_bytes + 64 > SMEM_BUDGET:
+    if NBUF * geo.buf_bytes + 64 > SMEM_BUDGET:
         return None
     return geo
 
@@ -181,10 +199,8 @@ class _Ctx:
         di, dj, dk = off
         wv = self.geo.wins.get(name)
         if wv is not None and dk == 0:
-            row = self.hi + di - wv.rlo
+            row = _phys(self.geo, wv, self.hi + di - wv.rlo)
             c = self.col + dj - wv.clo
-            if wv.kind == "stream":
-                return f"w_{name}[{row}][{c}]"
             return f"w_{name}[{row}][{c}]"
         # direct global load at the point (row r + hi + di, column j + col + dj)
         return (f"((double)GTS_AT(p.f_{name}, (r + {self.hi + di}), "
@@ -203,10 +219,12 @@ def _emit_point(stmt, ctx: _Ctx, ctype, api: set, out: list, indent: str, local:
         out.append(f"{indent}{{ const double v_ = {value};")
         wv = geo.wins.get(name)
         if wv is not None and wv.kind in ("temp", "own"):
-            row = ctx.hi - wv.rlo
+            row = _phys(geo, wv, ctx.hi - wv.rlo)
             c = ctx.col - wv.clo
             out.append(f"{indent}  w_{name}[{row}][{c}] = (double)({ctype[name]})(v_);")
-        if name in api:
+        if name in api and name in geo.buffered:
+            out.append(f"{indent}  o_{name}[{ctx.col}] = ({ctype[name]})(v_);")
+        elif name in api:
             out.append(f"{indent}  if (ok_{_cn(ctx.col)}) GTS_AT(p.f_{name}, r, (jl + {ctx.col}), kk) = ({ctype[name]})(v_);")
         elif name in ctx.arena:
             # arena copy for later launches: every point of the stage's extent
@@ -246,7 +264,7 @@ def emit(kname: str, plan, kplan, ctype: dict, dtypes: dict):
     out: list = []
     w = out.append
     tm = ", ".join(f"const __grid_constant__ CUtensorMap tm_{s.name}" for s in streams)
-    smem = 2 * geo.buf_bytes
+    smem = NBUF * geo.buf_bytes
     bar_off = smem
     w(f"// fused PARALLEL tile kernel: {TI}x{TJ} tile per k-plane, {NW} warps x {RI} rows, "
       f"{VJ} columns/lane; streamed {[s.name for s in streams]}, register windows "
@@ -256,7 +274,7 @@ def emit(kname: str, plan, kplan, ctype: dict, dtypes: dict):
     w("  extern __shared__ __align__(1024) unsigned char smem[];")
     w(f"  uint64_t* full = (uint64_t*)(smem + {bar_off});")
     w("  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;")
-    w("  if (threadIdx.x == 0) { gts_mbar_init(&full[0], 1); gts_mbar_init(&full[1], 1); gts_fence_mbar_init(); }")
+    w(f"  if (threadIdx.x == 0) {{ for (int b = 0; b < {NBUF}; ++b) gts_mbar_init(&full[b], 1); gts_fence_mbar_init(); }}")
     w("  __syncthreads();")
     w(f"  const int ni = p.ni, nj = p.nj;")
 
@@ -275,20 +293,22 @@ def emit(kname: str, plan, kplan, ctype: dict, dtypes: dict):
     for s in streams:
         w(f"  const int jsh_{s.name} = p.tsh_{s.name}_j, ish_{s.name} = p.tsh_{s.name}_i, ksh_{s.name} = p.tsh_{s.name}_k;")
     w("  int it = 0;")
-    w("  if (threadIdx.x == 0 && (int)blockIdx.x < ntiles) {")
-    issue("(int)blockIdx.x", 0)
+    w("  if (threadIdx.x == 0) {")
+    for m in range(NBUF - 1):
+        w(f"    if ((int)blockIdx.x + {m} * (int)gridDim.x < ntiles) {{")
+        issue(f"(int)blockIdx.x + {m} * (int)gridDim.x", m)
+        w("    }")
     w("  }")
     w("  for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {")
-    w("    const int buf = it & 1;")
-    w("    const uint32_t ph = (uint32_t)(it >> 1) & 1u;")
-    w("    // prefetch the next tile into the other buffer (freed at the end of the previous tile)")
-    w("    if (threadIdx.x == 0 && t + (int)gridDim.x < ntiles) {")
+    w(f"    const int buf = it % {NBUF};")
+    w(f"    const uint32_t ph = (uint32_t)(it / {NBUF}) & 1u;")
+    w(f"    // issue tile t + {NBUF - 1} grid strides ahead into the buffer freed by the last tile")
+    w(f"    if (threadIdx.x == 0 && t + {NBUF - 1} * (int)gridDim.x < ntiles) {{")
     w("      gts_fence_proxy_async();")
-    w("      if (buf == 0) {")
-    issue("t + (int)gridDim.x", 1)
-    w("      } else {")
-    issue("t + (int)gridDim.x", 0)
-    w("      }")
+    for b in range(NBUF):
+        w(f"      if ((it + {NBUF - 1}) % {NBUF} == {b}) {{")
+        issue(f"t + {NBUF - 1} * (int)gridDim.x", b)
+        w("      }")
     w("    }")
     w("    gts_mbar_wait(&full[buf], ph);")
     w("    const unsigned char* sb = smem + buf * " + str(geo.buf_bytes) + ";")
@@ -312,23 +332,38 @@ def emit(kname: str, plan, kplan, ctype: dict, dtypes: dict):
     nsteps = RI - steps_lo  # steps r = ra + min_step .. ra + RI - 1
 
     def load_stream_row(s, rowidx, rel_row):
-        # absolute row = r + rel_row; smem row = (r + rel_row) - (i0 + min_step + rlo)
-        for c in range(s.chi - s.clo + 1):
-            lane_col = f"(lane * {VJ} + {s.clo - s.bstart + c})"
-            w(f"      w_{s.name}[{rowidx}][{c}] = (double)sp_{s.name}[(size_t)((r + {rel_row}) - (i0 + {geo.min_step + s.rlo})) * {s.box_cols} + {lane_col}];")
+        # absolute row = r + rel_row; smem row = (r + rel_row) - (i0 + min_step + rlo);
+        # 8/16-B vector loads where the layout allows (rows are 16-B multiples)
+        off = s.clo - s.bstart
+        ncol = s.chi - s.clo + 1
+        rowexpr = f"(size_t)((r + {rel_row}) - (i0 + {geo.min_step + s.rlo})) * {s.box_cols}"
+        vmax = 16 // s.esize
+        c = 0
+        while c < ncol:
+            v = vmax
+            while v > 1 and not ((off + c) % v == 0 and VJ % v == 0 and c + v <= ncol):
+                v //= 2
+            idx = f"{rowexpr} + lane * {VJ} + {off + c}"
+            prow = _phys(geo, s, rowidx)
+            if v == 1:
+                w(f"      w_{s.name}[{prow}][{c}] = (double)sp_{s.name}[{idx}];")
+            else:
+                vt = {(8, 2): "double2", (4, 2): "float2", (4, 4): "float4"}[(s.esize, v)]
+                w(f"      {{ const {vt} q_ = *reinterpret_cast<const {vt}*>(sp_{s.name} + {idx});")
+                comps = "xyzw"
+                for q in range(v):
+                    w(f"        w_{s.name}[{prow}][{c + q}] = (double)q_.{comps[q]};")
+                w("      }")
+            c += v
 
     # fully unrolled steps (prologue + main)
     for step in range(nsteps):
         rel = steps_lo + step  # r = ra + rel
         w(f"    {{ // step r = ra + {rel}")
         w(f"      const int r = ra + {rel};")
-        # shift windows (rows move down by one)
-        if step > 0:
-            for x in regw + streams:
-                depth = x.rhi - x.rlo + 1
-                for d in range(depth - 1):
-                    w(f"      #pragma unroll")
-                    w(f"      for (int c = 0; c < {x.chi - x.clo + 1}; ++c) w_{x.name}[{d}][c] = w_{x.name}[{d + 1}][c];")
+        geo.rot = step  # windows slide by rotation, no moves
+        for f in sorted(geo.buffered):
+            w(f"      {ctype[f]} o_{f}[{VJ}];")
         # load stream rows: at the first step the whole window, later the top row
         for s in streams:
             if step == 0:
@@ -354,10 +389,28 @@ def emit(kname: str, plan, kplan, ctype: dict, dtypes: dict):
                     if wv is not None and wv.kind in ("temp", "own"):
                         # a conditionally written temporary reads as NaN where
                         # unwritten, like the reference's NaN-initialised ones
-                        w(f"          w_{f}[{hi - wv.rlo}][{col - wv.clo}] = GTS_NAN;")
+                        w(f"          w_{f}[{_phys(geo, wv, hi - wv.rlo)}][{col - wv.clo}] = GTS_NAN;")
                 _emit_point(st.body, ctx, ctype, api, out, "          ", local, geo)
                 w("        }")
             w("      }")
+        if rel >= 0:
+            # buffered api outputs: one row of VJ values per lane, vector store
+            for f in sorted(geo.buffered):
+                e = 8 if dtypes[f] == ir.F64 else 4
+                w(f"      if (r < ni) {{")
+                w(f"        {ctype[f]}* const op = &GTS_AT(p.f_{f}, r, jl, kk);")
+                w(f"        if (jl + {VJ} <= nj && p.f_{f}.sj == 1 && (((uintptr_t)op) & 15) == 0) {{")
+                if e == 8:
+                    for q in range(0, VJ, 2):
+                        w(f"          *reinterpret_cast<double2*>(op + {q}) = make_double2(o_{f}[{q}], o_{f}[{q + 1}]);")
+                else:
+                    for q in range(0, VJ, 4):
+                        w(f"          *reinterpret_cast<float4*>(op + {q}) = make_float4(o_{f}[{q}], o_{f}[{q + 1}], o_{f}[{q + 2}], o_{f}[{q + 3}]);")
+                w("        } else {")
+                for q in range(VJ):
+                    w(f"          if (jl + {q} < nj) op[(long long){q} * p.f_{f}.sj] = o_{f}[{q}];")
+                w("        }")
+                w("      }")
         w("    }")
     w("    __syncthreads();  // both buffers' readers done before the next prefetch reuses this one")
     w("  }")
@@ -386,9 +439,11 @@ def emit(kname: str, plan, kplan, ctype: dict, dtypes: dict):
         "      const int nkr = k1 - k0;",
         "      if (nkr > 0) {",
         "        const int ntiles = tiles_i * tiles_j * nkr;",
-        "        int grid = 2 * gts_sm_count(); if (grid > ntiles) grid = ntiles;",
         "        static bool attr = false;",
-        f"        if (!attr) {{ cudaFuncSetAttribute({kname}, cudaFuncAttributeMaxDynamicSharedMemorySize, {smem_bytes}); attr = true; }}",
+        "        static int per_sm = 1;",
+        f"        if (!attr) {{ cudaFuncSetAttribute({kname}, cudaFuncAttributeMaxDynamicSharedMemorySize, {smem_bytes});",
+        f"          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, {kname}, {32 * NW}, {smem_bytes}); if (per_sm < 1) per_sm = 1; attr = true; }}",
+        "        int grid = per_sm * gts_sm_count(); if (grid > ntiles) grid = ntiles;",
         f"        {kname}<<<grid, {32 * NW}, {smem_bytes}, st>>>(p, {tm_args}, k0, nkr, tiles_i, tiles_j, ntiles);",
         "      }",
         "    }",
