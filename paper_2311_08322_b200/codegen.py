@@ -352,7 +352,7 @@ def _point_kernel(kname: str, stage, ctype: dict, dtypes: dict) -> list:
 
 def generate_source(plan: Plan, fp, options: Optional[dict] = None) -> str:
     impl = plan.impl
-    from . import codegen_column, codegen_parallel  # template instantiations
+    from . import codegen_column, codegen_parallel, codegen_rowstream  # template instantiations
 
     opts = options or {}
 
@@ -415,7 +415,12 @@ def generate_source(plan: Plan, fp, options: Optional[dict] = None) -> str:
     for kidx, k in enumerate(plan.kernels):
         kname = f"gts_k{kidx}_{k.kind}"
         if k.kind == "pfused":
-            res = codegen_parallel.emit(kname, plan, k, ctype, dtypes) if opts.get("tma", True) else None
+            res = None
+            if opts.get("tma", True):
+                if opts.get("pf_mode", "tile") == "row":
+                    res = codegen_rowstream.emit(kname, plan, k, ctype, dtypes, opts)
+                else:
+                    res = codegen_parallel.emit(kname, plan, k, ctype, dtypes, opts)
             fb = []
             for r in k.stages:
                 nm = f"{kname}_s{r.idx}"

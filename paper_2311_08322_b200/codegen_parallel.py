@@ -251,7 +251,21 @@ def _emit_point(stmt, ctx: _Ctx, ctype, api: set, out: list, indent: str, local:
     raise TypeError(type(stmt).__name__)
 
 
-def emit(kname: str, plan, kplan, ctype: dict, dtypes: dict):
+DEFAULTS = {"pf_nw": 4, "pf_ri": 8, "pf_vj": 4, "pf_nbuf": 1}
+
+
+def configure(opts) -> None:
+    """Tile geometry (gen_options pf_nw / pf_ri / pf_vj / pf_nbuf; part of the
+    fingerprint like the reference gen engine's tile options, gen.py:235-238)."""
+    global NW, RI, VJ, TJ, TI, NBUF
+    o = dict(DEFAULTS)
+    o.update({k: v for k, v in (opts or {}).items() if k in DEFAULTS})
+    NW, RI, VJ, NBUF = int(o["pf_nw"]), int(o["pf_ri"]), int(o["pf_vj"]), int(o["pf_nbuf"])
+    TJ, TI = 32 * VJ, NW * RI
+
+
+def emit(kname: str, plan, kplan, ctype: dict, dtypes: dict, opts=None):
+    configure(opts)
     geo = eligible(plan, kplan, dtypes)
     if geo is None:
         return None
