@@ -375,6 +375,40 @@ def e2e_timed(st, kernel, dtype, domain, steps):
     return dt, h2d, d2h
 
 
+def decomposed_hdiff(dist, steps, warmup, tile=(512, 1024, 80)):
+    """C4: hdiff on a horizontally decomposed domain, a fixed 512x1024x80
+    tile per GPU (weak scaling; 2048x2048x80 at 8 GPUs on a 4x2 grid); each
+    step = NCCL halo exchange of inp overlapped with the interior + boundary
+    strips.  Returns (max-over-ranks ms per step, global domain, grid)."""
+    import paper_2311_08322_b200 as b200
+    from paper_2311_08322_b200 import decomp, native, workloads
+
+    grid = decomp.choose_grid(dist.world)
+    gdom = (tile[0] * grid[0], tile[1] * grid[1], tile[2])
+    d = decomp.Decomposition(gdom, grid, dist.rank)
+    ldom = d.local_domain
+    st = b200.compile_stencil(workloads.source("hdiff"), "hdiff")
+    rng = np.random.default_rng(1000 + dist.rank)
+    inp = b200.from_array(rng.uniform(-1, 1, (ldom[0] + 4, ldom[1] + 4, ldom[2])), (2, 2, 0))
+    out = b200.allocate("f64", ldom)
+    step = decomp.DecomposedStep(st, d, {"inp": inp, "out": out}, {"coeff": 0.05}, "inp", (2, 2))
+    stream = native.default_stream()
+    for _ in range(warmup):
+        step()
+    native.synchronize(stream)
+    e0, e1 = native.Event(), native.Event()
+    dist.barrier()
+    native.synchronize(stream)
+    e0.record(stream)
+    for _ in range(steps):
+        step()
+    e1.record(stream)
+    native.synchronize(stream)
+    dist.barrier()
+    ms = dist.max(e0.elapsed_ms(e1) / steps)
+    return ms, gdom, grid, step.launches_per_step
+
+
 def run_b200(args, dist):
     import paper_2311_08322_b200 as b200
     from paper_2311_08322_b200 import native, workloads
@@ -420,6 +454,24 @@ def run_b200(args, dist):
                      "peak_source": peak_src, "frac_of_8TBs_spec": achieved / 8000.0},
         "clocks": sampler.summary(),
     }
+    decomp_line = None
+    if not args.no_extra:
+        try:
+            ms_d, gdom, grid, lps = decomposed_hdiff(dist, max(args.steps // 4, 20), args.warmup)
+            pts_d = gdom[0] * gdom[1] * gdom[2]
+            alg_d = dist.world * workloads.algorithmic_bytes("hdiff", (512, 1024, 80), "f64")
+            decomp_line = {
+                "workload": "horizontal diffusion float64, 512x1024x80 per GPU, decomposed "
+                            f"{grid[0]}x{grid[1]} (global {gdom[0]}x{gdom[1]}x{gdom[2]}), NCCL halo "
+                            "exchange of inp overlapped with the interior",
+                "value": pts_d / (ms_d / 1e3), "unit": "grid-points/s", "ms_per_step": ms_d,
+                "achieved_gbs_per_gpu": alg_d / dist.world / (ms_d / 1e3) / 1e9,
+                "launches_per_step": lps, "scaling": "weak",
+            }
+        except Exception as exc:  # pragma: no cover - reported, not fatal
+            decomp_line = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+    if dist.rank == 0 and dist.world > 1:
+        line["extra"] = {"hdiff_decomposed": decomp_line}
     if dist.rank == 0 and dist.world == 1 and not args.no_extra:
         extra = {}
         for name in ("hdiff", "hdiff32"):
@@ -436,6 +488,7 @@ def run_b200(args, dist):
                 "parity": parity_check(k2, d2, r2["sets"]), "traffic": ncu_traffic(name),
                 "launches_per_step": r2["launches_per_step"],
             }
+        extra["hdiff_decomposed"] = decomp_line
         line["extra"] = extra
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
         cores, model = host_info()

@@ -102,10 +102,11 @@ class Module:
             native.check(self.lib.gts_b200_module_set_device(dev), "module set device")
             self._device = dev
 
-    def launcher(self, domain, fields: dict, scalars: dict, stream: int):
+    def launcher(self, domain, fields: dict, scalars: dict, stream: int, offset=(0, 0, 0)):
         """Pre-marshalled asynchronous launch over device-resident storages
-        ({name: DeviceFieldStorage}, origins = storage origins).  Returns a
-        zero-argument callable: one call = one enqueue of the stencil."""
+        ({name: DeviceFieldStorage}; origins = storage origins + ``offset``,
+        i.e. a sub-rectangle of the domain).  Returns a zero-argument
+        callable: one call = one enqueue of the stencil on ``stream``."""
         self.bind_device()
         args: list = [int(domain[0]), int(domain[1]), int(domain[2])]
         for name in self.field_order:
@@ -115,7 +116,7 @@ class Module:
             st.to_device(stream)
             args.append(st.base_address())
             args.extend(int(s) for s in st.strides)
-            args.extend(int(o) for o in st.origin)
+            args.extend(int(o) + int(d) for o, d in zip(st.origin, offset))
         for name in self.scalar_order:
             args.append(float(scalars[name]))
         args.append(stream)

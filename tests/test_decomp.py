@@ -1,0 +1,146 @@
+"""Horizontal decomposition + halo exchange (paper_2311_08322_b200/decomp.py).
+
+CPU part: world_size 2 and 4 over gloo (host transport) -- the rank grid,
+the two-phase face exchange (corners included) and the decomposed hdiff
+computed per rank with the C oracle equal to the undecomposed result.
+GPU part: the device pack/unpack kernels and strip-wise stencil calls on one
+B200, bitwise equal to the undecomposed run.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from paper_2311_08322_b200 import decomp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+def test_grid_covers_domain_once(world):
+    dom = (37, 29, 3)
+    grid = decomp.choose_grid(world)
+    assert grid[0] * grid[1] == world
+    seen = np.zeros(dom[:2], dtype=int)
+    for r in range(world):
+        d = decomp.Decomposition(dom, grid, r)
+        seen[d.i0: d.i1, d.j0: d.j1] += 1
+        for di, dj in ((-1, 0), (1, 0), (0, -1), (0, 1)):
+            nb = d.neighbour(di, dj)
+            if nb is not None:
+                e = decomp.Decomposition(dom, grid, nb)
+                assert (e.ri - d.ri, e.rj - d.rj) == (di, dj)
+    assert np.all(seen == 1)
+
+
+def test_strips_partition_local_domain():
+    for dom in [(12, 9, 2), (4, 4, 1), (5, 30, 3)]:
+        cover = np.zeros(dom[:2], dtype=int)
+        for _, (oi, oj), (si, sj, _) in decomp.strips(dom, (2, 2)):
+            cover[oi: oi + si, oj: oj + sj] += 1
+        assert np.all(cover == 1)
+
+
+def _worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle
+
+        glob_dom = (26, 21, 4)
+        rng = np.random.default_rng(42)
+        g_inp = rng.uniform(-1, 1, (glob_dom[0] + 4, glob_dom[1] + 4, glob_dom[2]))
+        d = decomp.Decomposition(glob_dom, decomp.choose_grid(world), rank)
+        local = d.scatter(g_inp, (2, 2))
+        want_halo = local.copy()
+        ni, nj, _ = d.local_domain
+        # poison every halo cell that a neighbour owns, keep global-boundary halos
+        poisoned = local.copy()
+        if d.neighbour(-1, 0) is not None:
+            poisoned[:2] = np.nan
+        if d.neighbour(1, 0) is not None:
+            poisoned[ni + 2:] = np.nan
+        if d.neighbour(0, -1) is not None:
+            poisoned[:, :2] = np.nan
+        if d.neighbour(0, 1) is not None:
+            poisoned[:, nj + 2:] = np.nan
+        ex = decomp.HaloExchanger(d, (2, 2), "f64", device=False)
+        ex.exchange(poisoned)
+        # hdiff needs no corner cells, but the two-phase exchange delivers them too
+        ok_halo = np.array_equal(poisoned, want_halo)
+        out_local = oracle.hdiff_c(poisoned, 0.05)
+        out_global = oracle.hdiff_c(g_inp, 0.05)
+        ok_out = np.array_equal(out_local, out_global[d.i0: d.i1, d.j0: d.j1])
+        q.put((rank, ok_halo, ok_out))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_gloo_halo_exchange_and_decomposed_hdiff(world):
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=180) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(ok_h and ok_o for _, ok_h, ok_o in res), res
+
+
+@pytest.mark.gpu
+def test_device_pack_unpack_and_strips_bitwise(gpu):
+    """Two sub-domains on one GPU: faces moved with the device pack/unpack
+    kernels, each sub-domain computed as interior + 4 strips; bitwise equal
+    to the undecomposed hdiff."""
+    import torch
+
+    import oracle
+    import paper_2311_08322_b200 as b200
+    from paper_2311_08322_b200 import native, workloads
+
+    glob_dom = (40, 70, 6)
+    rng = np.random.default_rng(7)
+    g_inp = rng.uniform(-1, 1, (glob_dom[0] + 4, glob_dom[1] + 4, glob_dom[2]))
+    st = b200.compile_stencil(workloads.source("hdiff"), "hdiff")
+    grid = (2, 1)
+    parts = []
+    for r in range(2):
+        d = decomp.Decomposition(glob_dom, grid, r)
+        local = d.scatter(g_inp, (2, 2))
+        if r == 0:
+            local[d.local_domain[0] + 2:] = np.nan  # owned by rank 1
+        else:
+            local[:2] = np.nan  # owned by rank 0
+        parts.append((d, b200.from_array(local, (2, 2, 0)), b200.allocate("f64", d.local_domain)))
+    ops = decomp._DeviceOps(torch, native.default_stream())
+    (d0, in0, _), (d1, in1, _) = parts
+    ni0, nj, nk = d0.local_domain
+    buf = torch.empty(2 * (nj + 4) * nk, dtype=torch.float64, device="cuda")
+    ops.pack(buf, in0, ((ni0, 0, 0), (2, nj + 4, nk)))  # rank 0 bottom interior rows
+    ops.unpack(in1, buf, ((0, 0, 0), (2, nj + 4, nk)))  # -> rank 1 top halo
+    ops.pack(buf, in1, ((2, 0, 0), (2, nj + 4, nk)))  # rank 1 top interior rows
+    ops.unpack(in0, buf, ((ni0 + 2, 0, 0), (2, nj + 4, nk)))  # -> rank 0 bottom halo
+    ops.synchronize()
+    in0.mark_device_written()
+    in1.mark_device_written()
+    want = oracle.hdiff_c(g_inp, 0.05)
+    for d, inp, out in parts:
+        for _, off, size in decomp.strips(d.local_domain, (2, 2)):
+            decomp.call_on_strip(st, {"inp": inp, "out": out}, {"coeff": 0.05}, off, size)
+        assert np.array_equal(out.host_array(), want[d.i0: d.i1, d.j0: d.j1])
