@@ -106,6 +106,15 @@ int gts_b200_unpack_box(void* base, const void* buf, int64_t s_i, int64_t s_j, i
                         int64_t i0, int64_t j0, int64_t k0, int64_t ni, int64_t nj, int64_t nk,
                         int itemsize, void* stream);
 
+/* CUDA graphs: capture everything enqueued on ``stream`` between begin and
+ * end (including generated-module entries and event records) into an
+ * executable graph; replay it with one launch.  Used for multi-step loops
+ * (the dycore step, the benchmark's timed region). */
+int gts_b200_graph_begin(void* stream);
+int gts_b200_graph_end(void* stream, void** exec);
+int gts_b200_graph_launch(void* exec, void* stream);
+int gts_b200_graph_destroy(void* exec);
+
 #ifdef __cplusplus
 }
 #endif

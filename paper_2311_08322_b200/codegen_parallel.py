@@ -252,20 +252,37 @@ def _emit_point(stmt, ctx: _Ctx, ctype, api: set, out: list, indent: str, local:
 
 
 DEFAULTS = {"pf_nw": 4, "pf_ri": 8, "pf_vj": 4, "pf_nbuf": 1}
+# Measured defaults per element size (profiles/sweep_hdiff_r1.md, hdiff
+# 256x256x80 on one B200, CUDA-graph timed):
+#  f64: 16x128 tiles, double-buffered TMA boxes: 16.9 us vs 18.1 us for
+#       32x128 single-buffered (HBM-bound; shorter tiles shrink the tail);
+#  f32: 16x128 tiles with 2 warps x 8 rows, double-buffered: FP64-pipe bound
+#       (f64 arithmetic on f32 storage), so fewer halo recomputations win.
+GEOMETRY = {8: {"pf_nw": 4, "pf_ri": 4, "pf_vj": 4, "pf_nbuf": 2},
+            4: {"pf_nw": 2, "pf_ri": 8, "pf_vj": 4, "pf_nbuf": 2}}
 
 
-def configure(opts) -> None:
+def configure(opts, esize: int = 0) -> None:
     """Tile geometry (gen_options pf_nw / pf_ri / pf_vj / pf_nbuf; part of the
-    fingerprint like the reference gen engine's tile options, gen.py:235-238)."""
+    fingerprint like the reference gen engine's tile options, gen.py:235-238).
+    Unset options take the measured default of the group's smallest streamed
+    element size ``esize`` (0: the generic DEFAULTS)."""
     global NW, RI, VJ, TJ, TI, NBUF
-    o = dict(DEFAULTS)
+    o = dict(GEOMETRY.get(esize, DEFAULTS))
     o.update({k: v for k, v in (opts or {}).items() if k in DEFAULTS})
     NW, RI, VJ, NBUF = int(o["pf_nw"]), int(o["pf_ri"]), int(o["pf_vj"]), int(o["pf_nbuf"])
     TJ, TI = 32 * VJ, NW * RI
 
 
+def _min_esize(plan, kplan, dtypes: dict) -> int:
+    api = {f.name for f in plan.impl.api_fields}
+    sizes = [8 if dtypes[a.field] == ir.F64 else 4
+             for r in kplan.stages for a in reads(r.stage.body) if a.field in api]
+    return min(sizes) if sizes else 0
+
+
 def emit(kname: str, plan, kplan, ctype: dict, dtypes: dict, opts=None):
-    configure(opts)
+    configure(opts, _min_esize(plan, kplan, dtypes))
     geo = eligible(plan, kplan, dtypes)
     if geo is None:
         return None

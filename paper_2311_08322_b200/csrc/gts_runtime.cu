@@ -82,6 +82,14 @@ GTS_EXPORT int gts_b200_event_destroy(void* event) {
   return (int)cudaEventDestroy((cudaEvent_t)event);
 }
 GTS_EXPORT int gts_b200_event_record(void* event, void* stream) {
+  // Inside a stream capture a plain record is only an intra-graph dependency
+  // marker; record "external" so the graph gets a real event-record node and
+  // the event keeps its timestamp semantics on every replay.
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing((cudaStream_t)stream, &cs);
+  if (cs == cudaStreamCaptureStatusActive)
+    return (int)cudaEventRecordWithFlags((cudaEvent_t)event, (cudaStream_t)stream,
+                                         cudaEventRecordExternal);
   return (int)cudaEventRecord((cudaEvent_t)event, (cudaStream_t)stream);
 }
 GTS_EXPORT int gts_b200_event_synchronize(void* event) {
@@ -180,4 +188,36 @@ GTS_EXPORT int gts_b200_unpack_box(void* base, const void* buf, int64_t s_i, int
                                    int64_t s_k, int64_t i0, int64_t j0, int64_t k0, int64_t ni,
                                    int64_t nj, int64_t nk, int itemsize, void* stream) {
   return box<false>((void*)buf, base, s_i, s_j, s_k, i0, j0, k0, ni, nj, nk, itemsize, stream);
+}
+
+// ---------------------------------------------------------------------------
+// CUDA graphs: capture a sequence of enqueues on a stream (generated module
+// entries, pack/unpack, event records) once and replay it with one launch --
+// removes the per-launch host cost from multi-step runs (the
+// 100-step dycore loop; bench.py's timed loop).  Capture is a property of
+// the driver stream, so launches made by the generated modules' own CUDA
+// runtimes on the same stream are captured too.
+// ---------------------------------------------------------------------------
+GTS_EXPORT int gts_b200_graph_begin(void* stream) {
+  return (int)cudaStreamBeginCapture((cudaStream_t)stream, cudaStreamCaptureModeThreadLocal);
+}
+
+GTS_EXPORT int gts_b200_graph_end(void* stream, void** exec) {
+  cudaGraph_t g = nullptr;
+  cudaError_t e = cudaStreamEndCapture((cudaStream_t)stream, &g);
+  if (e != cudaSuccess) return (int)e;
+  cudaGraphExec_t x = nullptr;
+  e = cudaGraphInstantiateWithFlags(&x, g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) return (int)e;
+  *exec = (void*)x;
+  return 0;
+}
+
+GTS_EXPORT int gts_b200_graph_launch(void* exec, void* stream) {
+  return (int)cudaGraphLaunch((cudaGraphExec_t)exec, (cudaStream_t)stream);
+}
+
+GTS_EXPORT int gts_b200_graph_destroy(void* exec) {
+  return (int)cudaGraphExecDestroy((cudaGraphExec_t)exec);
 }

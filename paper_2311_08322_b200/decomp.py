@@ -79,8 +79,10 @@ class Decomposition:
         """This rank's storage box (local domain + halo) of a global logical
         array laid out with the same halo (global storage coordinates)."""
         hi, hj = halo
-        return np.ascontiguousarray(
-            global_storage_array[self.i0: self.i1 + 2 * hi, self.j0: self.j1 + 2 * hj, :])
+        # always a copy: a slice of full trailing extent is already contiguous,
+        # and ascontiguousarray would hand back a view aliasing the global array
+        return np.array(
+            global_storage_array[self.i0: self.i1 + 2 * hi, self.j0: self.j1 + 2 * hj, :], copy=True)
 
 
 class _HostOps:

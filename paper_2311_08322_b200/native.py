@@ -51,6 +51,10 @@ SIGNATURES = {
     "gts_b200_l2_flush": (_INT, [_VP]),
     "gts_b200_pack_box": (_INT, [_VP, _VP] + [_I64] * 9 + [_INT, _VP]),
     "gts_b200_unpack_box": (_INT, [_VP, _VP] + [_I64] * 9 + [_INT, _VP]),
+    "gts_b200_graph_begin": (_INT, [_VP]),
+    "gts_b200_graph_end": (_INT, [_VP, _c.POINTER(_VP)]),
+    "gts_b200_graph_launch": (_INT, [_VP, _VP]),
+    "gts_b200_graph_destroy": (_INT, [_VP]),
 }
 
 _lib: Optional[ctypes.CDLL] = None
@@ -209,3 +213,48 @@ class Event:
 
 def l2_flush(stream: Optional[int] = None) -> None:
     call("gts_b200_l2_flush", stream if stream is not None else default_stream())
+
+
+class Graph:
+    """A captured sequence of enqueues on one stream, replayed with a single
+    launch (``gts_b200_graph_*``).  Use as::
+
+        g = Graph(stream)
+        with g.capture():
+            launcher(); launcher(); ...
+        g.launch()
+    """
+
+    def __init__(self, stream: Optional[int] = None):
+        self.stream = stream if stream is not None else default_stream()
+        self.ptr = None
+
+    def capture(self):
+        graph = self
+
+        class _Cap:
+            def __enter__(self_):
+                call("gts_b200_graph_begin", graph.stream)
+                return graph
+
+            def __exit__(self_, et, ev, tb):
+                p = ctypes.c_void_p()
+                st = lib().gts_b200_graph_end(graph.stream, ctypes.byref(p))
+                if et is None:
+                    check(st, "gts_b200_graph_end")
+                    graph.ptr = p.value
+                return False
+
+        return _Cap()
+
+    def launch(self) -> None:
+        if self.ptr is None:
+            raise BackendError(Code.TOOLCHAIN_MISSING, "graph launched before capture")
+        call("gts_b200_graph_launch", self.ptr, self.stream)
+
+    def __del__(self):  # pragma: no cover - best effort
+        try:
+            if self.ptr and _lib is not None:
+                _lib.gts_b200_graph_destroy(self.ptr)
+        except Exception:
+            pass
