@@ -216,3 +216,40 @@ def make_diagonally_dominant(rng: np.random.Generator, shape):
     b = np.abs(a) + np.abs(c) + rng.uniform(0.5, 1.5, shape)
     d = rng.uniform(-1.0, 1.0, shape)
     return a, b, c, d
+
+
+# ---------------------------------------------------------------------------
+# dycore step (BASELINE.json configs[4]; paper_2311_08322_b200/kernels/dycore.gts)
+# ---------------------------------------------------------------------------
+
+
+def dycore_update_np(x: np.ndarray, tau: float) -> np.ndarray:
+    """The interval-specialised update of dycore.gts (last computation):
+    [0,1) and [K-1,K): u_out = x; [1,K-1): u_out = x + tau*((x[k+1] - 2*x) + x[k-1])
+    -- the IR's left-to-right association (binary ops parse left-assoc, as in
+    the reference frontend), f64 IEEE ops, no contraction."""
+    u = x.copy()
+    if x.shape[2] > 2:
+        xm, x0, xp = x[:, :, :-2], x[:, :, 1:-1], x[:, :, 2:]
+        u[:, :, 1:-1] = x0 + tau * ((xp - 2.0 * x0) + xm)
+    return u
+
+
+def dycore_step(u: np.ndarray, a, b, c, coeff: float = 0.05, tau: float = 0.2) -> np.ndarray:
+    """One dycore.gts step on logical arrays: u is (ni+4, nj+4, nk) with its
+    halo; returns u_out on the compute domain (ni, nj, nk).  Composition of
+    the C restatements of hdiff (hdiff.gts:3-15) and the Thomas solve
+    (vadv.gts:4-16, d := the diffused field) and the numpy update above --
+    the multistage order of the reference engines (debug.py:301-355)."""
+    uh = hdiff_c(u, coeff)
+    x = vadv_c(a, b, c, uh)
+    return dycore_update_np(x, tau)
+
+
+def dycore_run(u: np.ndarray, a, b, c, steps: int, coeff: float = 0.05, tau: float = 0.2) -> np.ndarray:
+    """``steps`` steps with the host swap of dycore.gts (u_out becomes the next
+    u_in; the 2-cell halo keeps its initial values: Dirichlet boundary)."""
+    u = np.array(u, copy=True)
+    for _ in range(steps):
+        u[2:-2, 2:-2, :] = dycore_step(u, a, b, c, coeff, tau)
+    return u

@@ -199,7 +199,9 @@ GTS_EXPORT int gts_b200_unpack_box(void* base, const void* buf, int64_t s_i, int
 // runtimes on the same stream are captured too.
 // ---------------------------------------------------------------------------
 GTS_EXPORT int gts_b200_graph_begin(void* stream) {
-  return (int)cudaStreamBeginCapture((cudaStream_t)stream, cudaStreamCaptureModeThreadLocal);
+  // relaxed: a generated module may cudaMalloc its persistent temporary
+  // arena while the first step is being captured (gts_common.cuh gts_arena)
+  return (int)cudaStreamBeginCapture((cudaStream_t)stream, cudaStreamCaptureModeRelaxed);
 }
 
 GTS_EXPORT int gts_b200_graph_end(void* stream, void** exec) {

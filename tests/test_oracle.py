@@ -86,3 +86,26 @@ def test_reference_ref_kernels_present_or_skipped():
         pytest.skip("oracle/_ref not built here")
     m = json.loads(man.read_text())
     assert set(m) == {"hdiff_f64", "hdiff_f32", "vadv_f64", "vadv_f32"}
+
+
+def _dycore_cases():
+    g = np.load(GOLDEN / "dycore.npz")
+    keys = sorted({k.rsplit("_", 1)[0] for k in g.files})
+    return g, keys
+
+
+def test_dycore_oracle_matches_reference_engines_bitwise():
+    """oracle.dycore_run (C hdiff + C Thomas + numpy update) vs the
+    reference's vec/debug engines running kernels/dycore.gts with the host
+    swap (tests/golden/make_golden_dycore.py)."""
+    from paper_2311_08322_b200 import workloads
+
+    g, keys = _dycore_cases()
+    assert keys
+    for key in keys:
+        dom = tuple(int(x) for x in key.split("_")[1].split("x"))
+        u, a, b, c = (workloads.dycore_arrays(dom, int(g[key + "_seed"]))[n] for n in "uabc")
+        state = u.copy()
+        for s in range(int(g[key + "_steps"])):
+            state[2:-2, 2:-2, :] = oracle.dycore_step(state, a, b, c, 0.05, 0.2)
+            assert np.array_equal(state[2:-2, 2:-2, :], g[f"{key}_out{s}"]), (key, s)
