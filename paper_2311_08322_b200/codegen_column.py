@@ -47,7 +47,7 @@ SMEM_MAX = 232448  # max dynamic shared memory per CTA on sm_100a
 class ThomasSpec:
     ms_f: int
     ms_b: int
-    streamed: list  # api fields streamed through the TMA ring (forward reads)
+    streamed: list  # fields streamed through the TMA ring (forward reads): api fields / arena temps
     cross: list  # temps written in forward, read in backward -> TMEM
     words: dict  # temp -> 32-bit words per level
     offsets: dict  # temp -> word offset within a level
@@ -55,18 +55,54 @@ class ThomasSpec:
     stage_bytes: int
     offs_in_stage: dict  # streamed field -> byte offset within a ring stage
     nstages: int
+    ms_e: Optional[int] = None  # fused PARALLEL epilogue multistage (zero extent)
+    ewin: tuple = ()  # backward-written fields the epilogue reads, via a register window
+    elo: int = 0  # window covers levels [m + elo, m + ehi] of epilogue level m
+    ehi: int = 0
+
+
+def _epilogue_ok(impl, mse, wf: set, wb: set, run_reads: set):
+    """A trailing PARALLEL multistage fused into the backward sweep: it may
+    read fields written by the backward sweep at vertical offsets (a register
+    window, level m computed once level m + lo is known), pure inputs at any
+    vertical offset (global loads) and its own temporaries at (0,0,0); it
+    writes api fields nobody else in the run reads, or its own temps."""
+    if mse.order != ir.PARALLEL:
+        return None
+    we = set()
+    for st in mse.stages:
+        we |= writes(st.body)
+    if we & (wf | wb):
+        return None
+    win, lo, hi = set(), 0, 0
+    for st in mse.stages:
+        for acc in reads(st.body):
+            di, dj, dk = acc.offset
+            if di or dj:
+                return None
+            if acc.field in wf:
+                return None  # forward temporaries are gone by then (TMEM reused)
+            if acc.field in wb:
+                if acc.field in {f.name for f in impl.api_fields}:
+                    return None  # api outputs of the sweep: no register copy kept
+                win.add(acc.field)
+                lo, hi = min(lo, dk), max(hi, dk)
+            elif acc.field in we and dk != 0:
+                return None
+    if we & run_reads:
+        return None
+    return tuple(sorted(win)), lo, hi
 
 
 def spec(plan, kplan, dtypes: dict) -> Optional[ThomasSpec]:
     impl = plan.impl
-    if kplan.kind != "column" or len(kplan.multistages) != 2:
+    if kplan.kind != "column" or len(kplan.multistages) not in (2, 3):
         return None
-    mf, mb = kplan.multistages
+    mf, mb = kplan.multistages[:2]
     msf, msb = impl.multistages[mf], impl.multistages[mb]
     if msf.order != ir.FORWARD or msb.order != ir.BACKWARD:
         return None
     api = {f.name for f in impl.api_fields}
-    temps = {t.name for t in impl.temporaries}
     wf, wb = set(), set()
     for st in msf.stages:
         wf |= writes(st.body)
@@ -74,12 +110,32 @@ def spec(plan, kplan, dtypes: dict) -> Optional[ThomasSpec]:
         wb |= writes(st.body)
     if wf & api:
         return None
-    if any(f in plan.global_temps and f in wb for f in wb):
-        return None  # backward temporaries must stay kernel-local
+    # readers outside this run: every temporary the run writes must stay
+    # kernel-local (the template keeps them in TMEM / registers only)
+    outside = set()
+    for mi, ms in enumerate(impl.multistages):
+        if mi in kplan.multistages:
+            continue
+        for st in ms.stages:
+            outside |= {a.field for a in reads(st.body)}
+    if (wf | wb) & outside & set(plan.global_temps):
+        return None
+    run_reads = set()
+    for ms in (msf, msb):
+        for st in ms.stages:
+            run_reads |= {a.field for a in reads(st.body)}
+    ms_e, ewin, elo, ehi = None, (), 0, 0
+    if len(kplan.multistages) == 3:
+        ms_e = kplan.multistages[2]
+        got = _epilogue_ok(impl, impl.multistages[ms_e], wf, wb, run_reads)
+        if got is None:
+            return None
+        ewin, elo, ehi = got
     streamed = []
     for st in msf.stages:
         for acc in reads(st.body):
-            if acc.field in api:
+            # api inputs, and arena temporaries produced by an earlier launch
+            if acc.field in api or (acc.field in plan.global_temps and acc.field not in wf | wb):
                 if acc.offset != (0, 0, 0) or acc.field in wb:
                     return None
                 if acc.field not in streamed:
@@ -92,11 +148,6 @@ def spec(plan, kplan, dtypes: dict) -> Optional[ThomasSpec]:
                     return None
                 if acc.field not in cross:
                     cross.append(acc.field)
-    # temporaries of the forward sweep read by later launches would need the
-    # arena: not supported by this template
-    for t in wf:
-        if t in plan.global_temps and t not in cross:
-            return None
     if not streamed:
         return None
     cross.sort()
@@ -113,7 +164,8 @@ def spec(plan, kplan, dtypes: dict) -> Optional[ThomasSpec]:
     nstages = max(2, min(MAX_STAGES, RING_BUDGET // sb))
     if nstages * sb > RING_BUDGET:
         return None
-    return ThomasSpec(mf, mb, streamed, cross, words, offsets, max(w, 1), sb, offs, nstages)
+    return ThomasSpec(mf, mb, streamed, cross, words, offsets, max(w, 1), sb, offs, nstages,
+                      ms_e, ewin, elo, ehi)
 
 
 class _Ctx(_MemCtx):
@@ -368,8 +420,10 @@ def _emit_variant(kname, plan, sp: ThomasSpec, v: Variant, ctype, dtypes, opts):
     w("      const bool valid = (i < p.ni) && (j < p.nj);")
     w("      const int ic = i < p.ni ? i : p.ni - 1, jc = j < p.nj ? j : p.nj - 1;")
     w("      (void)ic; (void)jc;")
+    mse = impl.multistages[sp.ms_e] if sp.ms_e is not None else None
+    epi_stages = list(mse.stages) if mse is not None else []
     for f in impl.api_fields:
-        if any(f.name in writes(st.body) for st in msb.stages):
+        if any(f.name in writes(st.body) for st in list(msb.stages) + epi_stages):
             w(f"      {ctype[f.name]}* const colp_{f.name} = &GTS_AT(p.f_{f.name}, ic, jc, 0);")
     cf = _caches(msf, 1)
     wf = set()
@@ -483,6 +537,42 @@ def _emit_variant(kname, plan, sp: ThomasSpec, v: Variant, ctype, dtypes, opts):
     ctx_b = _Ctx(dtypes, sp, "b", cached_b, ctype)
     need_load = {f: any(_need_load(stg, f) for _, stg in gb) for f in wb if f in api and f in cb}
 
+    # fused PARALLEL epilogue: level m = k - elo runs once the backward sweep
+    # has produced level k (the lowest level the epilogue reads); the fields
+    # it reads from the sweep sit in a register window ew_<f>_<d> = f(k + d)
+    ge = _interval_groups(mse) if mse is not None else []
+    D = sp.ehi - sp.elo
+    we_all = set()
+    for st in epi_stages:
+        we_all |= writes(st.body)
+    for gi, (iv, _) in enumerate(ge):
+        w(f"      const int e{gi}k0 = {_bound(iv.start)}, e{gi}k1 = {_bound(iv.end)};")
+    for f in sp.ewin:
+        for d in range(D + 1):
+            w(f"      double ew_{f}_{d} = GTS_NAN;")
+    ctx_e = _EpiCtx(dtypes, sp, ctype, we_all - api)
+
+    def epilogue_level(indent, shift_in):
+        """Shift the window (``shift_in``: the new level-k values) and run the
+        epilogue at level m = k - elo when it lies in [0, nk)."""
+        for f in sp.ewin:
+            for d in range(D, 0, -1):
+                w(f"{indent}ew_{f}_{d} = ew_{f}_{d - 1};")
+            w(f"{indent}ew_{f}_0 = {shift_in(f)};")
+        w(f"{indent}{{ const int m_ = k - ({sp.elo});")
+        w(f"{indent}  if (m_ >= 0 && m_ < nk) {{ const int k = m_;")
+        for t in sorted(we_all - api):
+            w(f"{indent}    double cur_{t} = GTS_NAN;")
+        for gi, (iv, stages) in enumerate(ge):
+            kw = "if" if gi == 0 else "else if"
+            w(f"{indent}    {kw} (k >= e{gi}k0 && k < e{gi}k1) {{")
+            ctx_e.pool = DivPool("branch")
+            for st in stages:
+                _emit_stmt(st.body, ctx_e, ctype, api, indent + "      ", out)
+            w(f"{indent}    }}")
+        w(f"{indent}  }}")
+        w(f"{indent}}}")
+
     def backward_level(indent, hist_value, group=None):
         for t in sp.cross:
             w(f"{indent}const double cur_{t} = {hist_value(t)};")
@@ -510,6 +600,8 @@ def _emit_variant(kname, plan, sp: ThomasSpec, v: Variant, ctype, dtypes, opts):
             for s_ in range(depth, 1, -1):
                 w(f"{indent}prev{s_}_{f} = prev{s_ - 1}_{f};")
             w(f"{indent}prev1_{f} = cur_{f};")
+        if mse is not None:
+            epilogue_level(indent, lambda f: f"cur_{f}")
 
     if dbg == "fwdonly":
         w("      if (nk > 100000) {")
@@ -587,6 +679,11 @@ def _emit_variant(kname, plan, sp: ThomasSpec, v: Variant, ctype, dtypes, opts):
     w("          }")
     w("        }")
     w("      }")
+    if mse is not None and sp.elo < 0:
+        # epilogue levels whose lowest read lies below level 0
+        w(f"      for (int k = -1; k >= {sp.elo}; --k) {{")
+        epilogue_level("        ", lambda f: "GTS_NAN")
+        w("      }")
     if dbg == "fwdonly":
         w("      }")
     w("      __syncwarp();")
@@ -609,6 +706,29 @@ def _emit_variant(kname, plan, sp: ThomasSpec, v: Variant, ctype, dtypes, opts):
         ]
 
     return out, None, call
+
+
+class _EpiCtx(_MemCtx):
+    """Reads inside the fused epilogue: backward-sweep outputs from the
+    register window, its own temporaries from cur_*, pure inputs from
+    global memory at (ic, jc, k + dk)."""
+
+    def __init__(self, dtypes, sp: ThomasSpec, ctype: dict, local: set):
+        super().__init__(dtypes)
+        self.sp, self.ctype, self.local = sp, ctype, set(local)
+        self.cached = {t: 0 for t in local}  # _emit_stmt keeps cur_<t> for these
+
+    def addr(self, name, off):
+        di, dj, dk = off
+        kk = f"(k{dk:+d})" if dk else "k"
+        return f"GTS_AT(p.f_{name}, ic, jc, {kk})"
+
+    def read(self, name, off):
+        if name in self.sp.ewin:
+            return f"ew_{name}_{off[2] - self.sp.elo}"
+        if name in self.local:
+            return f"cur_{name}"
+        return super().read(name, off)
 
 
 class _PrefCtx(_Ctx):
