@@ -106,6 +106,14 @@ int gts_b200_unpack_box(void* base, const void* buf, int64_t s_i, int64_t s_j, i
                         int64_t i0, int64_t j0, int64_t k0, int64_t ni, int64_t nj, int64_t nk,
                         int itemsize, void* stream);
 
+/* Pipelined mirror mode (host FieldStorages): strided 2-D copies (``height``
+ * rows of ``width`` bytes, pitches in bytes) and cross-stream ordering. */
+int gts_b200_memcpy2d_h2d(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width,
+                          size_t height, void* stream);
+int gts_b200_memcpy2d_d2h(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width,
+                          size_t height, void* stream);
+int gts_b200_stream_wait_event(void* stream, void* event);
+
 /* CUDA graphs: capture everything enqueued on ``stream`` between begin and
  * end (including generated-module entries and event records) into an
  * executable graph; replay it with one launch.  Used for multi-step loops

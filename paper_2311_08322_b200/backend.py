@@ -149,6 +149,147 @@ class Module:
             raise native.DeviceError(status, f"{self.symbol}")
 
 
+# bytes moved by the last mirror-mode call (bench.py's e2e line reports them)
+last_transfer: dict = {"h2d": 0, "d2h": 0, "chunks": 0}
+_events: list = []
+
+
+def _event(i: int):
+    while len(_events) <= i:
+        _events.append(native.Event())
+    return _events[i]
+
+
+def _interval_range(iv, nk: int) -> tuple:
+    def b(x):
+        return x.offset if x.ref == ir.START else nk + x.offset
+    return b(iv.start), b(iv.end)
+
+
+def _fully_written(impl, name: str, nk: int) -> bool:
+    """Some multistage assigns ``name`` unconditionally on every level
+    [0, nk) (so the device twin needs no upload of its old values)."""
+    from .lowering import always_writes
+
+    for ms in impl.multistages:
+        cover = []
+        for st in ms.stages:
+            if name in always_writes(st.body):
+                cover.append(_interval_range(st.interval, nk))
+        cover.sort()
+        reach = 0
+        for lo, hi in cover:
+            if lo > reach:
+                break
+            reach = max(reach, hi)
+        if reach >= nk:
+            return True
+    return False
+
+
+class _Pipeline:
+    """Mirror mode for host FieldStorages, pipelined over i-row chunks of the
+    domain: chunk c's input rows go host->device on one copy stream while
+    chunk c-1 computes and chunk c-2's outputs go device->host on the other
+    (PCIe is full duplex).  Legal when no api field is both read and written
+    and outputs do not alias inputs; a written field that the stencil
+    overwrites entirely (storage == domain, every level unconditionally
+    assigned) is never uploaded."""
+
+    CHUNK_ROWS = 32
+
+    def __init__(self, module, impl):
+        self.module, self.impl = module, impl
+        reads_ = set()
+        for ms in impl.multistages:
+            for st in ms.stages:
+                reads_ |= {a.field for a in ir.stmt_reads(st.body) if isinstance(a, ir.FieldAccess)}
+        self.inputs = [n for n in module.field_order if n not in module.written]
+        self.outputs = [n for n in module.field_order if n in module.written]
+        self.ok = not (set(self.outputs) & reads_)
+        self.ext = {n: impl.field_extent(n) for n in module.field_order}
+
+    def eligible(self, domain, field_args) -> bool:
+        if not self.ok or domain[0] < 2 * self.CHUNK_ROWS:
+            return False
+        outs = {id(field_args[n][0]._base) for n in self.outputs}
+        ins = {id(field_args[n][0]._base) for n in self.inputs}
+        if outs & ins or len(outs) != len(self.outputs):
+            return False
+        for n in self.module.field_order:
+            st = field_args[n][0]
+            if isinstance(st, DeviceFieldStorage) or st.strides[1] != 1:
+                return False
+            if st.strides[0] * st.shape[0] > st.strides[2] and st.shape[2] > 1:
+                return False
+        return True
+
+    def run(self, domain, field_args, scalar_args) -> None:
+        ni, nj, nk = domain
+        comp = native.default_stream()
+        up, down = native.aux_stream("h2d"), native.aux_stream("d2h")
+        mirrors, ptrs, strides, origins = {}, {}, {}, {}
+        for n in self.module.field_order:
+            st, org = field_args[n]
+            m = _mirror_for(st)
+            mirrors[n] = m
+            ptrs[n] = m.device_address(st)
+            strides[n] = tuple(int(x) for x in st.strides)
+            origins[n] = tuple(int(o) for o in org)
+        skip = {n for n in self.outputs
+                if tuple(field_args[n][0].shape) == tuple(domain) and origins[n] == (0, 0, 0)
+                and _fully_written(self.impl, n, nk)}
+        nch = max(1, ni // self.CHUNK_ROWS)
+        bounds = [(c * ni // nch, (c + 1) * ni // nch) for c in range(nch)]
+        done_row = {n: 0 for n in self.module.field_order}  # storage rows uploaded so far
+        h2d = d2h = 0
+
+        def copy(n, r0, r1, kind, stream):
+            st = field_args[n][0]
+            e = st.itemsize
+            r0, r1 = max(r0, 0), min(r1, st.shape[0])
+            if r1 <= r0:
+                return 0
+            width = (r1 - r0) * st.strides[0] * e
+            pitch = st.strides[2] * e if st.shape[2] > 1 else width
+            host = st.base_address() + r0 * st.strides[0] * e
+            dev = ptrs[n] + r0 * st.strides[0] * e
+            if kind == "h2d":
+                native.call("gts_b200_memcpy2d_h2d", dev, pitch, host, pitch, width, st.shape[2], stream)
+            else:
+                native.call("gts_b200_memcpy2d_d2h", host, pitch, dev, pitch, width, st.shape[2], stream)
+            return width * st.shape[2]
+
+        for c, (c0, c1) in enumerate(bounds):
+            last = c == nch - 1
+            for n in self.module.field_order:
+                if n in skip:
+                    continue
+                e = self.ext[n]
+                o = origins[n][0]
+                lo = o + c0 + (e.lo[0] if n in self.inputs else 0)
+                hi = o + c1 + (e.hi[0] if n in self.inputs else 0)
+                if last and n in self.inputs:
+                    hi = max(hi, field_args[n][0].shape[0])
+                lo = max(lo, done_row[n])
+                h2d += copy(n, lo, hi, "h2d", up)
+                done_row[n] = max(done_row[n], hi)
+            ev_in = _event(2 * c)
+            ev_in.record(up)
+            native.call("gts_b200_stream_wait_event", comp, ev_in.ptr)
+            org_c = {n: (origins[n][0] + c0, origins[n][1], origins[n][2]) for n in origins}
+            self.module.launch((c1 - c0, nj, nk), ptrs, strides, org_c, scalar_args, comp)
+            ev_done = _event(2 * c + 1)
+            ev_done.record(comp)
+            native.call("gts_b200_stream_wait_event", down, ev_done.ptr)
+            for n in self.outputs:
+                o = origins[n][0]
+                d2h += copy(n, o + c0, o + c1, "d2h", down)
+        native.synchronize(down)
+        native.synchronize(comp)
+        last_transfer.update(h2d=h2d, d2h=d2h, chunks=nch)
+
+
 def build(impl, fp, cache: Optional[BuildCache] = None, options: Optional[dict] = None):
     """Build (or fetch from the cache) and load the module for ``impl``."""
     cache = cache or BuildCache()
@@ -193,12 +334,18 @@ def build(impl, fp, cache: Optional[BuildCache] = None, options: Optional[dict] 
             origins[name] = tuple(int(o) for o in origin)
         return pointers, strides, origins, mirrors
 
+    pipe = _Pipeline(module, impl)
+
     def run(domain, field_args, scalar_args) -> None:
         if any(d == 0 for d in domain):
+            return
+        if pipe.eligible(domain, field_args):
+            pipe.run(domain, field_args, scalar_args)
             return
         stream = native.default_stream()
         pointers, strides, origins, mirrors = prepare(field_args, stream)
         module.launch(domain, pointers, strides, origins, scalar_args, stream)
+        last_transfer.update(h2d=sum(m.nbytes for m, _ in mirrors.values()), d2h=0, chunks=0)
         copied = set()
         for name in module.written:
             storage, _ = field_args[name]
@@ -211,6 +358,7 @@ def build(impl, fp, cache: Optional[BuildCache] = None, options: Optional[dict] 
                 copied.add(key)
                 m = mirrors[key][0]
                 native.call("gts_b200_memcpy_d2h", m.host_base, m.dptr, m.nbytes, stream)
+                last_transfer["d2h"] += m.nbytes
         native.synchronize(stream)
 
     build_info = {

@@ -412,9 +412,30 @@ def generate_source(plan: Plan, fp, options: Optional[dict] = None) -> str:
             "  }",
         ]
 
+    from . import codegen_prologue
+
+    skip = set()
     for kidx, k in enumerate(plan.kernels):
+        if kidx in skip:
+            continue
         kname = f"gts_k{kidx}_{k.kind}"
+        # a pfused group whose only product is consumed at the reader's own
+        # point by the next column run's forward sweep: fused into the TMEM
+        # column kernel as its prologue (codegen_prologue), with the two-launch
+        # form kept as the run-time fallback
+        fused_col = None
+        nxt = plan.kernels[kidx + 1] if kidx + 1 < len(plan.kernels) else None
+        if (k.kind == "pfused" and nxt is not None and nxt.kind == "column"
+                and opts.get("tmem", True) and opts.get("fuse_prologue", True)):
+            pro = codegen_prologue.prologue_spec(plan, k, nxt, dtypes)
+            if pro is not None:
+                sp_f = codegen_column.spec(plan, nxt, dtypes, pro)
+                if sp_f is not None:
+                    fused_col = sp_f
         if k.kind == "pfused":
+            saved_launches = launches
+            if fused_col is not None:
+                launches = []
             res = None
             if opts.get("tma", True):
                 if opts.get("pf_mode", "tile") == "row":
@@ -437,6 +458,23 @@ def generate_source(plan: Plan, fp, options: Optional[dict] = None) -> str:
                 fused_ok[kidx] = flag
                 prelude += pre
                 launches += [f"  if ({flag}) {{"] + launch + ["  } else {"] + fb + ["  }"]
+            if fused_col is not None:
+                pf_lines = launches
+                launches = saved_launches
+                cname = f"gts_k{kidx + 1}_column"
+                out.extend(_column_kernel(cname, plan, nxt, ctype, dtypes))
+                generic = [
+                    "  {",
+                    "    dim3 grid((unsigned)((nj + GTS_COL_TJ - 1) / GTS_COL_TJ),"
+                    " (unsigned)((ni + (GTS_COL_THREADS / GTS_COL_TJ) - 1) / (GTS_COL_THREADS / GTS_COL_TJ)), 1);",
+                    f"    {cname}<<<grid, GTS_COL_THREADS, 0, st>>>(p);",
+                    "  }",
+                ]
+                code, launch = codegen_column.emit(cname, plan, nxt, fused_col, ctype, dtypes, opts,
+                                                   fallback=pf_lines + generic)
+                out.extend(code)
+                launches += launch
+                skip.add(kidx + 1)
             w("")
             continue
         if k.kind == "pstage":

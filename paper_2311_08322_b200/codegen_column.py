@@ -29,11 +29,12 @@ aligned origin and byte strides); the entry falls back otherwise.
 
 from __future__ import annotations
 
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 from typing import Optional
 
 from ._host import ir
 from .codegen import DivPool, _bound, _interval_groups, _MemCtx, c_float, emit_expr  # noqa: F401
+from . import codegen_prologue
 from .lowering import always_writes, reads, writes
 
 KB = 8  # levels per TMA box (W=1 variant)
@@ -59,6 +60,30 @@ class ThomasSpec:
     ewin: tuple = ()  # backward-written fields the epilogue reads, via a register window
     elo: int = 0  # window covers levels [m + elo, m + ehi] of epilogue level m
     ehi: int = 0
+    pro: Optional[object] = None  # codegen_prologue.PrologueSpec fused in front of the forward sweep
+    halo: dict = field(default_factory=dict)  # prologue input -> HaloBox
+
+
+@dataclass
+class HaloBox:
+    """TMA box of a prologue input: tile + its horizontal halo, KB levels."""
+
+    lo_i: int
+    rows_extra: int  # hi_i - lo_i
+    cshift: int  # map base column lo_j - cshift is 16-B aligned
+    bstart: int  # box start column relative to the tile's first column (= lo_j - cshift)
+    cols: int  # box width (16-B multiple)
+    esize: int
+
+
+def _halo_box(ext, esize: int, rows: int) -> HaloBox:
+    lo_i, hi_i, lo_j, hi_j = ext
+    align = 16 // esize
+    cshift = lo_j % align
+    bstart = lo_j - cshift
+    cols = (TJ - 1 + hi_j) - bstart + 1
+    cols = -(-cols // align) * align
+    return HaloBox(lo_i, hi_i - lo_i, cshift, bstart, cols, esize)
 
 
 def _epilogue_ok(impl, mse, wf: set, wb: set, run_reads: set):
@@ -94,7 +119,9 @@ def _epilogue_ok(impl, mse, wf: set, wb: set, run_reads: set):
     return tuple(sorted(win)), lo, hi
 
 
-def spec(plan, kplan, dtypes: dict) -> Optional[ThomasSpec]:
+def spec(plan, kplan, dtypes: dict, pro=None) -> Optional[ThomasSpec]:
+    """``pro``: a PrologueSpec (codegen_prologue) to fuse in front of the
+    forward sweep; its exports are computed in-kernel instead of streamed."""
     impl = plan.impl
     if kplan.kind != "column" or len(kplan.multistages) not in (2, 3):
         return None
@@ -135,6 +162,11 @@ def spec(plan, kplan, dtypes: dict) -> Optional[ThomasSpec]:
     for st in msf.stages:
         for acc in reads(st.body):
             # api inputs, and arena temporaries produced by an earlier launch
+            # (unless a fused prologue computes them in-kernel)
+            if pro is not None and acc.field in pro.exports:
+                if acc.offset != (0, 0, 0):
+                    return None
+                continue
             if acc.field in api or (acc.field in plan.global_temps and acc.field not in wf | wb):
                 if acc.offset != (0, 0, 0) or acc.field in wb:
                     return None
@@ -148,8 +180,14 @@ def spec(plan, kplan, dtypes: dict) -> Optional[ThomasSpec]:
                     return None
                 if acc.field not in cross:
                     cross.append(acc.field)
-    if not streamed:
+    if not streamed and pro is None:
         return None
+    halo = {}
+    if pro is not None:
+        for f in pro.inputs:
+            if f in streamed:
+                return None  # read both with and without halo: not supported
+            halo[f] = pro.extent[f]
     cross.sort()
     words = {t: (2 if dtypes[t] == ir.F64 else 1) for t in cross}
     offsets, w = {}, 0
@@ -164,8 +202,13 @@ def spec(plan, kplan, dtypes: dict) -> Optional[ThomasSpec]:
     nstages = max(2, min(MAX_STAGES, RING_BUDGET // sb))
     if nstages * sb > RING_BUDGET:
         return None
+    for f in halo:  # capacity check with the W=1 geometry (the largest boxes per level)
+        hb = _halo_box(halo[f], 8 if dtypes[f] == ir.F64 else 4, TI)
+        sb += KB * (TI + hb.rows_extra) * hb.cols * hb.esize
+    if 2 * sb > RING_BUDGET:
+        return None
     return ThomasSpec(mf, mb, streamed, cross, words, offsets, max(w, 1), sb, offs, nstages,
-                      ms_e, ewin, elo, ehi)
+                      ms_e, ewin, elo, ehi, pro, halo)
 
 
 class _Ctx(_MemCtx):
@@ -184,7 +227,11 @@ class _Ctx(_MemCtx):
         kk = f"(k{dk:+d})" if dk else "k"
         return f"GTS_AT(p.f_{name}, {ii}, {jj}, {kk})"
 
+    pro_vals: dict = {}
+
     def read(self, name, off):
+        if self.phase == "f" and name in self.pro_vals and off == (0, 0, 0):
+            return self.pro_vals[name]
         if self.phase == "f" and self.ring and name in self.sp.streamed:
             return (f"((double)((const {self.ctype[name]}*)(sb + {self.offs[name]}))"
                     f"[(kk * {self.rows} + warp) * {TJ} + lane])")
@@ -275,6 +322,8 @@ class Variant:
     sl: int
     smem_bytes: int
     hist_off: int
+    hbox: dict = field(default_factory=dict)  # prologue input -> HaloBox for this geometry
+    tx: int = 0  # bytes the TMA boxes of one ring stage deliver (mbarrier expect-tx)
 
 
 def variants(sp: ThomasSpec, dtypes: dict) -> list:
@@ -287,6 +336,17 @@ def variants(sp: ThomasSpec, dtypes: dict) -> list:
         for f in sp.streamed:
             offs[f] = sb
             sb += kb * rows * TJ * esize[f]
+        tx = sb
+        hboxes = {}
+        for f, ext in sp.halo.items():
+            hb = _halo_box(ext, 8 if dtypes[f] == ir.F64 else 4, rows)
+            hboxes[f] = hb
+            sb = -(-sb // 128) * 128
+            offs[f] = sb
+            nb = kb * (rows + hb.rows_extra) * hb.cols * hb.esize
+            sb += nb
+            tx += nb
+        sb = -(-sb // 128) * 128
         nst = max(2, min(MAX_STAGES, budget // sb))
         ring = nst * sb
         nct = 32 * rows
@@ -296,18 +356,24 @@ def variants(sp: ThomasSpec, dtypes: dict) -> list:
         hist_off = ring
         smem = ring + sl * nct * hist_bytes + bars + 16
         tl = (512 // w) // sp.w_level
-        out.append(Variant(w, kb, nst, sb, offs, tl, sl, smem, hist_off))
+        if nst * sb > budget:
+            continue
+        out.append(Variant(w, kb, nst, sb, offs, tl, sl, smem, hist_off, hboxes, tx))
     return out
 
 
-def emit(kname: str, plan, kplan, sp: ThomasSpec, ctype: dict, dtypes: dict, opts=None):
+def emit(kname: str, plan, kplan, sp: ThomasSpec, ctype: dict, dtypes: dict, opts=None,
+         fallback=None):
+    """``fallback``: host lines run when no variant can launch (default: the
+    generic column kernel; with a fused prologue, the prologue's own launch
+    followed by the generic column kernel)."""
     code, launch_variants = [], []
     for v in variants(sp, dtypes):
         c, cond, call = _emit_variant(kname, plan, sp, v, ctype, dtypes, opts)
         code += c
         launch_variants.append((cond, call, v))
     launch = ["  {"]
-    for f in sp.streamed:
+    for f in list(sp.streamed) + list(sp.halo):
         launch.append(f"    CUtensorMap tm_{f}[2];")
     launch.append("    bool launched = false;")
     for vi, (cond, call, v) in enumerate(launch_variants):
@@ -318,19 +384,26 @@ def emit(kname: str, plan, kplan, sp: ThomasSpec, ctype: dict, dtypes: dict, opt
             launch.append(
                 f"      ok = ok && gts_make_tmap_3d(&tm_{f}[{vi}], (const void*)p.f_{f}.p, {e}, nj, ni, nk,"
                 f" p.f_{f}.si, p.f_{f}.sj, p.f_{f}.sk, {TJ}, {4 * v.w}, {v.kb});")
+        for f, hb in v.hbox.items():
+            lo_i, hi_i, lo_j, hi_j = sp.halo[f]
+            launch.append(
+                f"      ok = ok && gts_make_tmap_3d(&tm_{f}[{vi}], (const void*)&GTS_AT(p.f_{f}, {lo_i}, {hb.bstart}, 0),"
+                f" {hb.esize}, nj + {hi_j - hb.bstart}, ni + {hi_i - lo_i}, nk,"
+                f" p.f_{f}.si, p.f_{f}.sj, p.f_{f}.sk, {hb.cols}, {4 * v.w + hb.rows_extra}, {v.kb});")
         launch.append("      if (ok) {")
         launch += ["        " + ln for ln in call(vi)]
         launch.append("        launched = true;")
         launch.append("      }")
         launch.append("    }")
-    launch += [
-        "    if (!launched) {",
-        "      dim3 grid((unsigned)((nj + GTS_COL_TJ - 1) / GTS_COL_TJ),"
-        " (unsigned)((ni + (GTS_COL_THREADS / GTS_COL_TJ) - 1) / (GTS_COL_THREADS / GTS_COL_TJ)), 1);",
-        f"      {kname}<<<grid, GTS_COL_THREADS, 0, st>>>(p);",
-        "    }",
-        "  }",
-    ]
+    if fallback is None:
+        fallback = [
+            "  {",
+            "    dim3 grid((unsigned)((nj + GTS_COL_TJ - 1) / GTS_COL_TJ),"
+            " (unsigned)((ni + (GTS_COL_THREADS / GTS_COL_TJ) - 1) / (GTS_COL_THREADS / GTS_COL_TJ)), 1);",
+            f"    {kname}<<<grid, GTS_COL_THREADS, 0, st>>>(p);",
+            "  }",
+        ]
+    launch += ["    if (!launched) {"] + ["    " + ln for ln in fallback] + ["    }", "  }"]
     return code, launch
 
 
@@ -362,7 +435,8 @@ def _emit_variant(kname, plan, sp: ThomasSpec, v: Variant, ctype, dtypes, opts):
     assert v.tl % KB == 0
     out: list = []
     w = out.append
-    tm_params = ", ".join(f"const __grid_constant__ CUtensorMap tm_{f}" for f in sp.streamed)
+    tm_fields = list(sp.streamed) + list(sp.halo)
+    tm_params = ", ".join(f"const __grid_constant__ CUtensorMap tm_{f}" for f in tm_fields)
     w(f"// TMEM column kernel, W={v.w}: {nct} columns/CTA, streamed {sp.streamed} (ring {v.nst} x"
       f" {v.stage_bytes} B), history {sp.cross}: TMEM levels [0,{v.tl}), smem levels"
       f" [{v.tl},{v.tl + v.sl})")
@@ -390,7 +464,7 @@ def _emit_variant(kname, plan, sp: ThomasSpec, v: Variant, ctype, dtypes, opts):
     w(f"  const int nkb = (nk + {KB - 1}) / {KB};")
     w(f"  if (warp == {ncw}) {{")
     w("    if (lane == 0) {")
-    for f in sp.streamed:
+    for f in tm_fields:
         w(f"      gts_prefetch_tensormap(&tm_{f});")
     w("      int it = 0;")
     w("      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {")
@@ -399,8 +473,8 @@ def _emit_variant(kname, plan, sp: ThomasSpec, v: Variant, ctype, dtypes, opts):
     w("          const int s = it % NST;")
     w("          const uint32_t ph = (uint32_t)(it / NST) & 1u;")
     w("          if (it >= NST) gts_mbar_wait_sleep(&empty[s], ph ^ 1u);")
-    w("          gts_mbar_arrive_expect_tx(&full[s], STB);")
-    for f in sp.streamed:
+    w(f"          gts_mbar_arrive_expect_tx(&full[s], {v.tx}u);")
+    for f in tm_fields:
         w(f"          gts_tma_load_3d(smem + s * STB + {v.offs[f]}, &tm_{f}, &full[s], j0, i0, kb * {KB});")
     w("        }")
     w("      }")
@@ -451,6 +525,21 @@ def _emit_variant(kname, plan, sp: ThomasSpec, v: Variant, ctype, dtypes, opts):
         dispatch per level); tier: "tmem" / "smem" (None = per-level)."""
         for f in tracked_f:
             w(f"{indent}double cur_{f} = GTS_NAN;")
+        if sp.pro is not None:
+            # the fused PARALLEL prologue at this thread's (i, j, k)
+            if ctx.ring:
+                def rd(name, di, dj):
+                    hb = v.hbox[name]
+                    return (f"((const {ctype[name]}*)(sb + {v.offs[name]}))"
+                            f"[(kk * {rows + hb.rows_extra} + (warp + {di - hb.lo_i})) * {hb.cols}"
+                            f" + (lane + {dj - hb.bstart})]")
+            else:
+                def rd(name, di, dj):
+                    ii = f"(ic{di:+d})" if di else "ic"
+                    jj = f"(jc{dj:+d})" if dj else "jc"
+                    return f"GTS_AT(p.f_{name}, {ii}, {jj}, k)"
+            w(f"{indent}// fused prologue ({', '.join(sp.pro.exports)})")
+            ctx.pro_vals = codegen_prologue.emit_point(sp.pro, rd, ctype, out, indent)
         groups = [gf[group]] if group is not None else gf
         for gi, (iv, stages) in enumerate(groups):
             if group is None:
@@ -695,7 +784,7 @@ def _emit_variant(kname, plan, sp: ThomasSpec, v: Variant, ctype, dtypes, opts):
     w("}")
 
     def call(vi):
-        tm_args = ", ".join(f"tm_{f}[{vi}]" for f in sp.streamed)
+        tm_args = ", ".join(f"tm_{f}[{vi}]" for f in tm_fields)
         return [
             f"const int tiles_j = (int)((nj + {TJ - 1}) / {TJ});",
             f"const int ntiles = tiles_j * (int)((ni + {rows - 1}) / {rows});",

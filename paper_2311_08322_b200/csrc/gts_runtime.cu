@@ -223,3 +223,22 @@ GTS_EXPORT int gts_b200_graph_launch(void* exec, void* stream) {
 GTS_EXPORT int gts_b200_graph_destroy(void* exec) {
   return (int)cudaGraphExecDestroy((cudaGraphExec_t)exec);
 }
+
+// ---------------------------------------------------------------------------
+// Strided copies and cross-stream ordering for the pipelined mirror mode
+// (host FieldStorages): an i-row chunk of a k-outermost field is ``height``
+// = nk segments of ``width`` bytes, ``pitch`` bytes apart on both sides.
+// ---------------------------------------------------------------------------
+GTS_EXPORT int gts_b200_memcpy2d_h2d(void* dst, size_t dpitch, const void* src, size_t spitch,
+                                     size_t width, size_t height, void* stream) {
+  return (int)cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, height, cudaMemcpyHostToDevice,
+                                (cudaStream_t)stream);
+}
+GTS_EXPORT int gts_b200_memcpy2d_d2h(void* dst, size_t dpitch, const void* src, size_t spitch,
+                                     size_t width, size_t height, void* stream) {
+  return (int)cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, height, cudaMemcpyDeviceToHost,
+                                (cudaStream_t)stream);
+}
+GTS_EXPORT int gts_b200_stream_wait_event(void* stream, void* event) {
+  return (int)cudaStreamWaitEvent((cudaStream_t)stream, (cudaEvent_t)event, 0);
+}

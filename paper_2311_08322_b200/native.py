@@ -51,6 +51,9 @@ SIGNATURES = {
     "gts_b200_l2_flush": (_INT, [_VP]),
     "gts_b200_pack_box": (_INT, [_VP, _VP] + [_I64] * 9 + [_INT, _VP]),
     "gts_b200_unpack_box": (_INT, [_VP, _VP] + [_I64] * 9 + [_INT, _VP]),
+    "gts_b200_memcpy2d_h2d": (_INT, [_VP, _SZ, _VP, _SZ, _SZ, _SZ, _VP]),
+    "gts_b200_memcpy2d_d2h": (_INT, [_VP, _SZ, _VP, _SZ, _SZ, _SZ, _VP]),
+    "gts_b200_stream_wait_event": (_INT, [_VP, _VP]),
     "gts_b200_graph_begin": (_INT, [_VP]),
     "gts_b200_graph_end": (_INT, [_VP, _c.POINTER(_VP)]),
     "gts_b200_graph_launch": (_INT, [_VP, _VP]),
@@ -160,6 +163,20 @@ def require_device() -> int:
     if device_count() < 1:
         raise DeviceError(100, "no CUDA device visible to the b200 backend")
     return current_device()
+
+
+_aux_streams: dict = {}
+
+
+def aux_stream(name: str) -> int:
+    """Extra non-blocking streams per device (the mirror-mode copy engines)."""
+    dev = require_device()
+    s = _aux_streams.get((dev, name))
+    if s is None:
+        p = ctypes.c_void_p()
+        call("gts_b200_stream_create", ctypes.byref(p))
+        s = _aux_streams[(dev, name)] = p.value
+    return s
 
 
 def default_stream() -> int:

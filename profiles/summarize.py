@@ -19,7 +19,7 @@ OUT = HERE.parent / "gpurun_out"
 sys.path.insert(0, str(HERE))
 from ncu_summary import KEYS  # noqa: E402
 
-CAPTURES = {"vadv": "vadv_{r}", "hdiff": "hdiff64_{r}", "hdiff32": "hdiff32_{r}"}
+CAPTURES = {"vadv": "vadv_{r}", "hdiff": "hdiff64_{r}", "hdiff32": "hdiff32_{r}", "dycore": "dycore_{r}"}
 
 
 def raw(path):

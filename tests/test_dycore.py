@@ -70,3 +70,28 @@ def test_dycore_timeloop_graph_matches_oracle(gpu):
     want2 = oracle.dycore_run(want, arr["a"], arr["b"], arr["c"], steps)
     final2 = (A, B)[(2 * steps) % 2]
     assert np.array_equal(final2.host_array(), want2)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("opts,align", [
+    ({"fuse_prologue": False}, 128),  # hdiff launch + TMEM column kernel streaming uh
+    ({"tmem": False}, 128),           # hdiff launch + generic column kernel
+    ({}, 8),                          # TMA-incompatible storages: run-time fallback chain
+])
+def test_dycore_launch_paths_match_golden(gpu, opts, align):
+    import paper_2311_08322_b200 as b200
+    from paper_2311_08322_b200 import workloads
+    from paper_2311_08322_b200.storage import LayoutSpec
+
+    g = np.load(GOLDEN / "dycore.npz")
+    key = "dycore_24x20x16"
+    dom = (24, 20, 16)
+    st = b200.compile_stencil(workloads.source("dycore"), "dycore", gen_options=opts or None)
+    lay = LayoutSpec((2, 0, 1), align)
+    arr = workloads.dycore_arrays(dom, int(g[key + "_seed"]))
+    bufs = [b200.from_array(arr["u"], (2, 2, 0), lay), b200.from_array(arr["u"], (2, 2, 0), lay)]
+    coef = {n: b200.from_array(arr[n], (0, 0, 0), lay) for n in "abc"}
+    for s in range(int(g[key + "_steps"])):
+        src, dst = bufs[s % 2], bufs[(s + 1) % 2]
+        st(u_in=src, u_out=dst, **coef, **workloads.DYCORE_SCALARS)
+        assert np.array_equal(dst.host_array()[2:-2, 2:-2, :], g[f"{key}_out{s}"]), (opts, align, s)
