@@ -187,6 +187,38 @@ def _fully_written(impl, name: str, nk: int) -> bool:
     return False
 
 
+def _call_local(impl, name: str, nk: int) -> bool:
+    """Every read of ``name`` sees a value this call wrote: it is read only
+    inside the sequential multistage that assigns it unconditionally on every
+    level, at offsets (0, 0, dk) behind the sweep (FORWARD dk < 0, BACKWARD
+    dk > 0) -- vadv's ``x[0, 0, 1]`` in its BACKWARD sweep (vadv.gts:16)."""
+    from .lowering import always_writes
+
+    home = None
+    for mi, ms in enumerate(impl.multistages):
+        for st in ms.stages:
+            for acc in ir.stmt_reads(st.body):
+                if not isinstance(acc, ir.FieldAccess) or acc.field != name:
+                    continue
+                di, dj, dk = acc.offset
+                direction = {ir.FORWARD: 1, ir.BACKWARD: -1}.get(ms.order)
+                if direction is None or di or dj or dk * direction >= 0:
+                    return False
+                if home not in (None, mi):
+                    return False
+                home = mi
+    if home is None:
+        return True
+    ms = impl.multistages[home]
+    cover = sorted(_interval_range(st.interval, nk) for st in ms.stages if name in always_writes(st.body))
+    reach = 0
+    for lo, hi in cover:
+        if lo > reach:
+            return False
+        reach = max(reach, hi)
+    return reach >= nk
+
+
 class _Pipeline:
     """Mirror mode for host FieldStorages, pipelined over i-row chunks of the
     domain: chunk c's input rows go host->device on one copy stream while
@@ -206,11 +238,13 @@ class _Pipeline:
                 reads_ |= {a.field for a in ir.stmt_reads(st.body) if isinstance(a, ir.FieldAccess)}
         self.inputs = [n for n in module.field_order if n not in module.written]
         self.outputs = [n for n in module.field_order if n in module.written]
-        self.ok = not (set(self.outputs) & reads_)
+        self.read_outputs = set(self.outputs) & reads_
         self.ext = {n: impl.field_extent(n) for n in module.field_order}
 
     def eligible(self, domain, field_args) -> bool:
-        if not self.ok or domain[0] < 2 * self.CHUNK_ROWS:
+        if domain[0] < 2 * self.CHUNK_ROWS:
+            return False
+        if not all(_call_local(self.impl, n, domain[2]) for n in self.read_outputs):
             return False
         outs = {id(field_args[n][0]._base) for n in self.outputs}
         ins = {id(field_args[n][0]._base) for n in self.inputs}
