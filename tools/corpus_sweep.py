@@ -1,0 +1,89 @@
+"""Criterion-1 sweep over ALL 200 corpus programs on the GPU (evidence run).
+
+    python tools/corpus_sweep.py [N] > gpurun_out/corpus_sweep.json
+
+Compiles every program with a process pool (nvcc on the box, cache under
+/tmp so the repo snapshot stays small), then runs each one on cuda:0 with
+the reference harness inputs (tests/_inputs.py restatement of
+corpus.random_field_args) and compares SHA-256 of every output compute view
+with the reference debug engine's (tests/golden/corpus.json).  Also runs
+each program through three launch configurations (default, no fusion, no
+TMEM) to cover every lowering path.
+"""
+import json
+import os
+import sys
+import time
+from concurrent.futures import ProcessPoolExecutor
+from pathlib import Path
+
+REPO = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(REPO))
+sys.path.insert(0, str(REPO / "tests"))
+CACHE = "/tmp/gts_corpus_cache"
+OPTS = [None, {"fuse_parallel": False}, {"tmem": False, "tma": False}]
+
+
+def _compile(args):
+    idx, src, name, oi = args
+    import paper_2311_08322_b200 as b200
+
+    t0 = time.time()
+    try:
+        st = b200.compile_stencil(src, name, cache_dir=CACHE, gen_options=OPTS[oi])
+        return idx, oi, st.build_info["plan"], None, time.time() - t0
+    except Exception as exc:  # reported
+        return idx, oi, None, f"{type(exc).__name__}: {exc}"[:300], time.time() - t0
+
+
+def main():
+    n = int(sys.argv[1]) if len(sys.argv) > 1 else 200
+    print(json.dumps(sweep(n), indent=1))
+
+
+def sweep(n: int = 200, configs=None) -> dict:
+    meta = json.loads((REPO / "tests" / "golden" / "corpus.json").read_text())[:n]
+    cfgs = range(len(OPTS)) if configs is None else configs
+    jobs = [(e["idx"], e["source"], e["name"], oi) for e in meta for oi in cfgs]
+    t0 = time.time()
+    with ProcessPoolExecutor(max_workers=os.cpu_count() or 8) as ex:
+        comp = {(i, oi): (plan, err) for i, oi, plan, err, _ in ex.map(_compile, jobs)}
+    t_comp = time.time() - t0
+    import numpy as np
+    import _inputs
+    import paper_2311_08322_b200 as b200
+
+    results, kinds = [], {}
+    for e in meta:
+        for oi in cfgs:
+            plan, err = comp[(e["idx"], oi)]
+            rec = {"idx": e["idx"], "opts": OPTS[oi], "plan": plan}
+            if err:
+                rec["status"] = "compile_error"
+                rec["error"] = err
+                results.append(rec)
+                continue
+            st = b200.compile_stencil(e["source"], e["name"], cache_dir=CACHE, gen_options=OPTS[oi])
+            dom = tuple(e["domain"])
+            arrays = _inputs.random_field_arrays(st.implementation, dom, np.random.default_rng(e["seed"]))
+            fields = {k: b200.from_array(a, o) for k, (a, o) in arrays.items()}
+            try:
+                st(domain=dom, **fields, **e["scalars"])
+                ok = all(_inputs.sha(_inputs.compute_view(fields[o].host_array(), fields[o].origin, dom))
+                         == e["output_sha"][o] for o in e["outputs"])
+                rec["status"] = "bitwise" if ok else "MISMATCH"
+            except Exception as exc:
+                rec["status"] = "run_error"
+                rec["error"] = f"{type(exc).__name__}: {exc}"[:300]
+            for k in plan:
+                kinds[k.split(":")[0]] = kinds.get(k.split(":")[0], 0) + 1
+            results.append(rec)
+    summary = {"programs": len(meta), "configs": len(list(cfgs)), "compile_s": round(t_comp, 1),
+               "status": {}, "kernel_kinds": kinds}
+    for r in results:
+        summary["status"][r["status"]] = summary["status"].get(r["status"], 0) + 1
+    return {"summary": summary, "failures": [r for r in results if r["status"] != "bitwise"]}
+
+
+if __name__ == "__main__":
+    main()
