@@ -368,7 +368,10 @@ def emit(kname: str, plan, kplan, sp: ThomasSpec, ctype: dict, dtypes: dict, opt
     generic column kernel; with a fused prologue, the prologue's own launch
     followed by the generic column kernel)."""
     code, launch_variants = [], []
+    only_w = (opts or {}).get("tmem_w")  # gen_options: restrict to one geometry (experiments)
     for v in variants(sp, dtypes):
+        if only_w and v.w != int(only_w):
+            continue
         c, cond, call = _emit_variant(kname, plan, sp, v, ctype, dtypes, opts)
         code += c
         launch_variants.append((cond, call, v))
@@ -459,6 +462,8 @@ def _emit_variant(kname, plan, sp: ThomasSpec, v: Variant, ctype, dtypes, opts):
     w("  gts_tmem_fence_before_sync();")
     w("  __syncthreads();")
     w("  gts_tmem_fence_after_sync();")
+    w("  gts_griddep_launch_dependents();")
+    w("  gts_griddep_wait();  // PDL: previous grid complete before any global access")
     w("  const uint32_t tbase = *tslot;")
     w("  const int nk = p.nk;")
     w(f"  const int nkb = (nk + {KB - 1}) / {KB};")
@@ -600,7 +605,9 @@ def _emit_variant(kname, plan, sp: ThomasSpec, v: Variant, ctype, dtypes, opts):
     w("        __syncwarp();")
     w("        if (lane == 0) gts_mbar_arrive(&empty[s]);")
     w("      }")
-    w("      if (__any_sync(0xffffffffu, bad_)) {")
+    # columns outside the domain (TMA zero-fill of a partial tile) never force
+    # the exact replay: their values are never stored
+    w("      if (__any_sync(0xffffffffu, bad_ && valid)) {")
     for f, depth in sorted(cf.items()):
         for s_ in range(1, depth + 1):
             w(f"        prev{s_}_{f} = GTS_NAN;")
@@ -791,7 +798,7 @@ def _emit_variant(kname, plan, sp: ThomasSpec, v: Variant, ctype, dtypes, opts):
             "int grid = gts_sm_count(); if (grid > ntiles) grid = ntiles;",
             f"static bool attr_w{v.w} = false;",
             f"if (!attr_w{v.w}) {{ cudaFuncSetAttribute({kn}, cudaFuncAttributeMaxDynamicSharedMemorySize, {v.smem_bytes}); attr_w{v.w} = true; }}",
-            f"{kn}<<<grid, {threads}, {v.smem_bytes}, st>>>(p, {tm_args}, tiles_j, ntiles);",
+            f"gts_launch_pdl({kn}, dim3(grid), dim3({threads}), {v.smem_bytes}, st, p, {tm_args}, tiles_j, ntiles);",
         ]
 
     return out, None, call

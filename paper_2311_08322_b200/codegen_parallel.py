@@ -251,7 +251,7 @@ def _emit_point(stmt, ctx: _Ctx, ctype, api: set, out: list, indent: str, local:
     raise TypeError(type(stmt).__name__)
 
 
-DEFAULTS = {"pf_nw": 4, "pf_ri": 8, "pf_vj": 4, "pf_nbuf": 1}
+DEFAULTS = {"pf_nw": 4, "pf_ri": 8, "pf_vj": 4, "pf_nbuf": 1}  # + pf_pdl: off|early|late
 # Measured defaults per element size (profiles/sweep_hdiff_r1.md, hdiff
 # 256x256x80 on one B200, CUDA-graph timed):
 #  f64: 16x128 tiles, double-buffered TMA boxes: 16.9 us vs 18.1 us for
@@ -307,6 +307,11 @@ def emit(kname: str, plan, kplan, ctype: dict, dtypes: dict, opts=None):
     w("  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;")
     w(f"  if (threadIdx.x == 0) {{ for (int b = 0; b < {NBUF}; ++b) gts_mbar_init(&full[b], 1); gts_fence_mbar_init(); }}")
     w("  __syncthreads();")
+    pdl = (opts or {}).get("pf_pdl", "off")  # measured: early-trigger PDL slows 256^2 hdiff
+    if pdl == "early":
+        w("  gts_griddep_launch_dependents();")
+    if pdl != "off":
+        w("  gts_griddep_wait();  // PDL: previous grid complete before any global access")
     w(f"  const int ni = p.ni, nj = p.nj;")
 
     def issue(tvar, buf):
@@ -331,6 +336,8 @@ def emit(kname: str, plan, kplan, ctype: dict, dtypes: dict, opts=None):
         w("    }")
     w("  }")
     w("  for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {")
+    if pdl == "late":
+        w("    if (t + (int)gridDim.x >= ntiles) gts_griddep_launch_dependents();  // last tile of this CTA")
     w(f"    const int buf = it % {NBUF};")
     w(f"    const uint32_t ph = (uint32_t)(it / {NBUF}) & 1u;")
     w(f"    // issue tile t + {NBUF - 1} grid strides ahead into the buffer freed by the last tile")
@@ -475,7 +482,9 @@ def emit(kname: str, plan, kplan, ctype: dict, dtypes: dict, opts=None):
         f"        if (!attr) {{ cudaFuncSetAttribute({kname}, cudaFuncAttributeMaxDynamicSharedMemorySize, {smem_bytes});",
         f"          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, {kname}, {32 * NW}, {smem_bytes}); if (per_sm < 1) per_sm = 1; attr = true; }}",
         "        int grid = per_sm * gts_sm_count(); if (grid > ntiles) grid = ntiles;",
-        f"        {kname}<<<grid, {32 * NW}, {smem_bytes}, st>>>(p, {tm_args}, k0, nkr, tiles_i, tiles_j, ntiles);",
+        (f"        gts_launch_pdl({kname}, dim3(grid), dim3({32 * NW}), {smem_bytes}, st, p, {tm_args}, k0, nkr, tiles_i, tiles_j, ntiles);"
+         if pdl != "off" else
+         f"        {kname}<<<grid, {32 * NW}, {smem_bytes}, st>>>(p, {tm_args}, k0, nkr, tiles_i, tiles_j, ntiles);"),
         "      }",
         "    }",
     ]

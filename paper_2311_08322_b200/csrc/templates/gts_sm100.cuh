@@ -174,6 +174,38 @@ __device__ __forceinline__ void gts_tmem_store_f32(uint32_t taddr, float v) {
 }
 
 // ---------------------------------------------------------------------------
+// Programmatic dependent launch (PDL): a persistent stencil kernel lets the
+// next launch in the stream start as soon as every CTA of this one is
+// resident, and waits for the previous grid's completion (and memory flush)
+// before its first global access -- the next kernel's launch latency and
+// setup (mbarrier init, TMEM alloc, tensor-map prefetch) overlap this one's
+// tail.  Kernels that call gts_griddep_wait() before touching global memory
+// are launched through gts_launch_pdl(); all others keep full serialisation.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void gts_griddep_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+__device__ __forceinline__ void gts_griddep_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+template <typename... KArgs, typename... Args>
+static cudaError_t gts_launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                                  cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, ((KArgs)args)...);
+}
+
+// ---------------------------------------------------------------------------
 // Host: tensor maps
 // ---------------------------------------------------------------------------
 typedef CUresult (*gts_encode_tiled_fn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
