@@ -62,6 +62,7 @@ class ThomasSpec:
     ehi: int = 0
     pro: Optional[object] = None  # codegen_prologue.PrologueSpec fused in front of the forward sweep
     halo: dict = field(default_factory=dict)  # prologue input -> HaloBox
+    coop: bool = True  # materialize multi-offset prologue temps cooperatively in smem
 
 
 @dataclass
@@ -324,6 +325,9 @@ class Variant:
     hist_off: int
     hbox: dict = field(default_factory=dict)  # prologue input -> HaloBox for this geometry
     tx: int = 0  # bytes the TMA boxes of one ring stage deliver (mbarrier expect-tx)
+    mat: dict = field(default_factory=dict)  # materialized prologue temp -> (smem offset in a set, rows, cols, esize, region)
+    mat_off: int = 0  # smem offset of the two materialization buffer sets
+    mat_half: int = 0  # bytes of one set
 
 
 def variants(sp: ThomasSpec, dtypes: dict) -> list:
@@ -350,15 +354,24 @@ def variants(sp: ThomasSpec, dtypes: dict) -> list:
         nst = max(2, min(MAX_STAGES, budget // sb))
         ring = nst * sb
         nct = 32 * rows
+        # cooperative prologue: temporaries materialized per ring stage in two
+        # alternating shared-memory sets (codegen_prologue.materialized)
+        mat, half = {}, 0
+        if sp.pro is not None and sp.coop:
+            for t, (li, hi, lj, hj) in codegen_prologue.materialized(sp.pro).items():
+                e = 8 if dtypes[t] == ir.F64 else 4
+                rr, cc = rows + hi - li, TJ + hj - lj
+                mat[t] = (half, rr, cc, e, (li, hi, lj, hj))
+                half += -(-(kb * rr * cc * e) // 128) * 128
         bars = 2 * 8 * nst + 16
-        free = SMEM_MAX - ring - bars - 64
+        free = SMEM_MAX - ring - 2 * half - bars - 64
         sl = max(0, free // (nct * hist_bytes))
-        hist_off = ring
-        smem = ring + sl * nct * hist_bytes + bars + 16
+        hist_off = ring + 2 * half
+        smem = ring + 2 * half + sl * nct * hist_bytes + bars + 16
         tl = (512 // w) // sp.w_level
         if nst * sb > budget:
             continue
-        out.append(Variant(w, kb, nst, sb, offs, tl, sl, smem, hist_off, hboxes, tx))
+        out.append(Variant(w, kb, nst, sb, offs, tl, sl, smem, hist_off, hboxes, tx, mat, ring, half))
     return out
 
 
@@ -369,6 +382,9 @@ def emit(kname: str, plan, kplan, sp: ThomasSpec, ctype: dict, dtypes: dict, opt
     followed by the generic column kernel)."""
     code, launch_variants = [], []
     only_w = (opts or {}).get("tmem_w")  # gen_options: restrict to one geometry (experiments)
+    # cooperative materialization measured slower (235 vs 179 us/step: the per-stage
+    # consumer barrier serialises the 8 warps), so it is opt-in
+    sp.coop = bool((opts or {}).get("pro_coop", False)) and bool((opts or {}).get("pro_batch", True))
     for v in variants(sp, dtypes):
         if only_w and v.w != int(only_w):
             continue
@@ -525,26 +541,84 @@ def _emit_variant(kname, plan, sp: ThomasSpec, v: Variant, ctype, dtypes, opts):
                 w(f"{indent}  (({ctype[t]}*)(hl + {hoff[t]}))[ct] = ({ctype[t]})cur_{t};")
             w(f"{indent}}}")
 
-    def forward_level(ctx, indent, group=None, tier=None):
+    def prologue_rd(ring: bool):
+        if ring:
+            def rd(name, di, dj):
+                hb = v.hbox[name]
+                return (f"((const {ctype[name]}*)(sb + {v.offs[name]}))"
+                        f"[(kk * {rows + hb.rows_extra} + (warp + {di - hb.lo_i})) * {hb.cols}"
+                        f" + (lane + {dj - hb.bstart})]")
+        else:
+            def rd(name, di, dj):
+                ii = f"(ic{di:+d})" if di else "ic"
+                jj = f"(jc{dj:+d})" if dj else "jc"
+                return f"GTS_AT(p.f_{name}, {ii}, {jj}, k)"
+        return rd
+
+    pro_batch = sp.pro is not None and (opts or {}).get("pro_batch", True)
+
+    def mat_reads():
+        """Phase-B spellings of the materialized temps (this stage's set)."""
+        reads_ = {}
+        for t, (off, rr, cc, e, (li, hi, lj, hj)) in v.mat.items():
+            def rd(di, dj, off=off, rr=rr, cc=cc, li=li, lj=lj, t=t):
+                return (f"((const {ctype[t]}*)(smem + {v.mat_off} + (it & 1) * {v.mat_half} + {off}))"
+                        f"[(kk * {rr} + (warp + {di - li})) * {cc} + (lane + {dj - lj})]")
+            reads_[t] = rd
+        return reads_
+
+    def coop_phase(indent):
+        """Phase A: every consumer thread computes a share of each
+        materialized temp over the tile + its halo for the KB levels of
+        this stage; one named barrier (consumers only) publishes them.  Two
+        alternating sets make a second barrier unnecessary: a set is reused
+        two stages later, after every consumer passed the next barrier."""
+        for t, (off, rr, cc, e, (li, hi, lj, hj)) in v.mat.items():
+            n = KB * rr * cc
+            w(f"{indent}{{ {ctype[t]}* const mb_ = ({ctype[t]}*)(smem + {v.mat_off} + (it & 1) * {v.mat_half} + {off});")
+            w(f"{indent}  for (int q_ = ct; q_ < {n}; q_ += {nct}) {{")
+            w(f"{indent}    const int kk = q_ / {rr * cc}, rem_ = q_ - kk * {rr * cc};")
+            w(f"{indent}    const int r_ = rem_ / {cc} + ({li}), c_ = rem_ % {cc} + ({lj});")
+
+            def rd(name, di, dj):
+                hb = v.hbox[name]
+                return (f"((const {ctype[name]}*)(sb + {v.offs[name]}))"
+                        f"[(kk * {rows + hb.rows_extra} + (r_ + {di - hb.lo_i})) * {hb.cols}"
+                        f" + (c_ + {dj - hb.bstart})]")
+            w(f"{indent}    double mv_;")
+            codegen_prologue.emit_stage_value(sp.pro, t, rd, ctype, out, indent + "    ", "mv_")
+            w(f"{indent}    mb_[q_] = ({ctype[t]})mv_;")
+            w(f"{indent}  }}")
+            w(f"{indent}}}")
+        w(f'{indent}asm volatile("bar.sync 1, {nct};" ::: "memory");')
+
+    def prologue_batch(indent):
+        """The fused prologue for all KB levels of a full ring stage up front
+        (independent of the recurrence: the scheduler can overlap it)."""
+        if v.mat:
+            coop_phase(indent)
+        for f in sp.pro.exports:
+            w(f"{indent}double pv_{f}[{KB}];")
+        w(f"{indent}#pragma unroll")
+        w(f"{indent}for (int kk = 0; kk < {KB}; ++kk) {{")
+        vals = codegen_prologue.emit_point(sp.pro, prologue_rd(True), ctype, out, indent + "  ",
+                                           mat_read=mat_reads())
+        for f, var in vals.items():
+            w(f"{indent}  pv_{f}[kk] = {var};")
+        w(f"{indent}}}")
+
+    def forward_level(ctx, indent, group=None, tier=None, batched=False):
         """group: index of the statically known interval group (None =
-        dispatch per level); tier: "tmem" / "smem" (None = per-level)."""
+        dispatch per level); tier: "tmem" / "smem" (None = per-level);
+        batched: the prologue values were computed by prologue_batch."""
         for f in tracked_f:
             w(f"{indent}double cur_{f} = GTS_NAN;")
-        if sp.pro is not None:
+        if batched:
+            ctx.pro_vals = {f: f"pv_{f}[kk]" for f in sp.pro.exports}
+        elif sp.pro is not None:
             # the fused PARALLEL prologue at this thread's (i, j, k)
-            if ctx.ring:
-                def rd(name, di, dj):
-                    hb = v.hbox[name]
-                    return (f"((const {ctype[name]}*)(sb + {v.offs[name]}))"
-                            f"[(kk * {rows + hb.rows_extra} + (warp + {di - hb.lo_i})) * {hb.cols}"
-                            f" + (lane + {dj - hb.bstart})]")
-            else:
-                def rd(name, di, dj):
-                    ii = f"(ic{di:+d})" if di else "ic"
-                    jj = f"(jc{dj:+d})" if dj else "jc"
-                    return f"GTS_AT(p.f_{name}, {ii}, {jj}, k)"
             w(f"{indent}// fused prologue ({', '.join(sp.pro.exports)})")
-            ctx.pro_vals = codegen_prologue.emit_point(sp.pro, rd, ctype, out, indent)
+            ctx.pro_vals = codegen_prologue.emit_point(sp.pro, prologue_rd(ctx.ring), ctype, out, indent)
         groups = [gf[group]] if group is not None else gf
         for gi, (iv, stages) in enumerate(groups):
             if group is None:
@@ -588,12 +662,18 @@ def _emit_variant(kname, plan, sp: ThomasSpec, v: Variant, ctype, dtypes, opts):
             kw = "if" if first else "} else if"
             first = False
             w(f"        {kw} (fullst && {tcond} && kbase >= f{gi}k0 && kbase + {KB} <= f{gi}k1) {{")
+            if pro_batch:
+                prologue_batch("          ")
             w("          #pragma unroll")
             w(f"          for (int kk = 0; kk < {KB}; ++kk) {{")
             w("            const int k = kbase + kk;")
-            forward_level(ctx_f, "            ", gi, tier)
+            forward_level(ctx_f, "            ", gi, tier, batched=pro_batch)
             w("          }")
     w("        } else {")
+    if pro_batch and v.mat:
+        # one consumer barrier per stage on every path keeps the two
+        # materialization sets' reuse distance safe (see coop_phase)
+        w(f'          asm volatile("bar.sync 1, {nct};" ::: "memory");')
     w("          #pragma unroll")
     w(f"          for (int kk = 0; kk < {KB}; ++kk) {{")
     w("            const int k = kbase + kk;")

@@ -142,6 +142,41 @@ def prologue_spec(plan, kpf, kcol, dtypes: dict):
                         {f: sorted(v) for f, v in req.items()})
 
 
+def materialized(ps: PrologueSpec) -> dict:
+    """Temporaries worth computing ONCE per tile point into shared memory
+    instead of per thread at every required offset: those evaluated at >= 3
+    offsets (hdiff's ``lap``: the 5-point cross) whose stage reads only the
+    group's inputs.  Returns temp -> (lo_i, hi_i, lo_j, hi_j) of the offsets."""
+    out = {}
+    for st in ps.stages:
+        outs = writes(st.body)
+        if len(outs) != 1:
+            continue
+        t = next(iter(outs))
+        offs = ps.required.get(t, [])
+        if len(offs) < 3:
+            continue
+        if any(a.field in ps.required for a in reads(st.body)):
+            continue
+        out[t] = (min(o[0] for o in offs), max(o[0] for o in offs),
+                  min(o[1] for o in offs), max(o[1] for o in offs))
+    return out
+
+
+def emit_stage_value(ps: PrologueSpec, name: str, read_input, ctype: dict, out: list, indent: str,
+                     target: str) -> None:
+    """The stage that writes temp ``name``, evaluated at the point whose
+    inputs ``read_input(input, di, dj)`` spells, assigned to C variable
+    ``target`` (narrowed to the temp's type)."""
+    for st in ps.stages:
+        if name in writes(st.body):
+            ctx = _PointCtx(ps, read_input, 0, 0)
+            ctx.rename = {name: target}
+            _emit_stmt(st.body, ctx, ctype, out, indent)
+            return
+    raise KeyError(name)
+
+
 def _vn(name: str, oi: int, oj: int) -> str:
     def s(x):
         return f"m{-x}" if x < 0 else str(x)
@@ -151,22 +186,29 @@ def _vn(name: str, oi: int, oj: int) -> str:
 class _PointCtx:
     """Reads of one stage evaluated at horizontal offset (oi, oj)."""
 
-    def __init__(self, ps: PrologueSpec, read_input, oi: int, oj: int):
+    def __init__(self, ps: PrologueSpec, read_input, oi: int, oj: int, mat_read=None):
         self.ps, self.read_input, self.oi, self.oj = ps, read_input, oi, oj
         self.pool = None
+        self.rename = {}
+        self.mat_read = mat_read or {}
 
     def read(self, name, off):
         di, dj, _ = off
+        if name in self.mat_read:
+            return f"((double){self.mat_read[name](self.oi + di, self.oj + dj)})"
         if name in self.ps.required:
             return _vn(name, self.oi + di, self.oj + dj)
         return f"((double){self.read_input(name, self.oi + di, self.oj + dj)})"
+
+    def target(self, name):
+        return self.rename.get(name) or _vn(name, self.oi, self.oj)
 
 
 def _emit_stmt(stmt, ctx, ctype: dict, out: list, indent: str) -> None:
     if isinstance(stmt, ir.Assign):
         name = stmt.target.field
         value = emit_expr(stmt.value, ctx)
-        out.append(f"{indent}{_vn(name, ctx.oi, ctx.oj)} = (double)({ctype[name]})({value});")
+        out.append(f"{indent}{ctx.target(name)} = (double)({ctype[name]})({value});")
         return
     if isinstance(stmt, ir.If):
         out.append(f"{indent}if ({emit_expr(stmt.cond, ctx)}) {{")
@@ -181,20 +223,28 @@ def _emit_stmt(stmt, ctx, ctype: dict, out: list, indent: str) -> None:
     raise TypeError(type(stmt).__name__)
 
 
-def emit_point(ps: PrologueSpec, read_input, ctype: dict, out: list, indent: str) -> dict:
+def emit_point(ps: PrologueSpec, read_input, ctype: dict, out: list, indent: str,
+               mat_read=None) -> dict:
     """Straight-line evaluation of the group at the thread's own point.
     ``read_input(name, di, dj)`` spells a read of an input at a horizontal
-    offset.  Returns {export: C variable holding its value}."""
+    offset; ``mat_read`` {temp: f(di, dj)} spells reads of temporaries
+    already materialized in shared memory (their stages are skipped).
+    Returns {export: C variable holding its value}."""
+    mat_read = mat_read or {}
     for f, offs in sorted(ps.required.items()):
+        if f in mat_read:
+            continue
         for (oi, oj) in offs:
             out.append(f"{indent}double {_vn(f, oi, oj)};")
     for st in ps.stages:
+        if writes(st.body) & set(mat_read):
+            continue
         offs = set()
         for g in writes(st.body):
             offs |= set(ps.required[g])
         for (oi, oj) in sorted(offs):
-            _emit_stmt(st.body, _PointCtx(ps, read_input, oi, oj), ctype, out, indent)
+            _emit_stmt(st.body, _PointCtx(ps, read_input, oi, oj, mat_read), ctype, out, indent)
     return {f: _vn(f, 0, 0) for f in ps.exports}
 
 
-__all__ = ["PrologueSpec", "prologue_spec", "emit_point", "c_float"]
+__all__ = ["PrologueSpec", "prologue_spec", "emit_point", "materialized", "emit_stage_value", "c_float"]
