@@ -233,6 +233,43 @@ def time_reference(kernel, dtype, domain, seconds: float, max_calls: int, warmup
     return times
 
 
+def cpu_rows(kernel, dtype, domain, cores, seconds=4.0):
+    """SURVEY.md 8(d) secondary CPU rows: the gen kernel on 1 thread, and the
+    reference's NumPy engine (vec) through its own compile_stencil."""
+    rows = {}
+    pts = domain[0] * domain[1] * domain[2]
+    os.environ["GTS_NUM_THREADS"] = "1"  # read by the generated C on every call (gen.py:296-299)
+    try:
+        t1 = time_reference(kernel, dtype, domain, seconds=seconds, max_calls=50, warmup=1)
+        if t1:
+            rows["gen_1_thread"] = {"value": pts / statistics.median(t1), "calls": len(t1),
+                                    "median_call_ms": statistics.median(t1) * 1e3}
+    finally:
+        os.environ["GTS_NUM_THREADS"] = str(cores)
+    try:
+        import paper_2311_08322_b200  # noqa: F401  (locates stencilforge)
+        from stencilforge import bench as sf_bench
+        from stencilforge import runtime as sf_rt
+        from stencilforge.kernels import kernel_source
+
+        src = kernel_source(kernel)
+        if dtype == "f32":
+            src = src.replace("Field[f64]", "Field[f32]")
+        st = sf_rt.compile_stencil(src, kernel, backend="vec")
+        a = sf_bench.KERNEL_BUILDERS[kernel]("vec", tuple(domain), 0)
+        st(**a)
+        tv, t_end = [], time.perf_counter() + seconds
+        while not tv or (time.perf_counter() < t_end and len(tv) < 20):
+            t0 = time.perf_counter()
+            st(**a)
+            tv.append(time.perf_counter() - t0)
+        rows["vec_numpy_1_thread"] = {"value": pts / statistics.median(tv), "calls": len(tv),
+                                      "median_call_ms": statistics.median(tv) * 1e3}
+    except Exception as exc:  # pragma: no cover - reported, not fatal
+        rows["vec_numpy_1_thread"] = {"error": f"{type(exc).__name__}: {exc}"[:200]}
+    return rows
+
+
 def run_reference(args, dist):
     if dist.rank != 0:
         return
@@ -580,7 +617,9 @@ def run_b200(args, dist):
                 "sample": f"{len(times)} full {domain[0]}x{domain[1]}x{domain[2]} calls (median) of the "
                           f"reference gen engine's own generated C kernel (oracle/_ref), OpenMP over "
                           f"{cores} host threads ({model}), ~{args.cpu_seconds:.0f} s",
+                "min_call_ms": min(times) * 1e3, "median_call_ms": statistics.median(times) * 1e3,
             }
+            line["cpu_baseline"]["rows"] = cpu_rows(kernel, dtype, domain, cores)
     if dist.rank == 0:
         print(json.dumps(line))
 

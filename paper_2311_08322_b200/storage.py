@@ -266,3 +266,16 @@ def pinned_host_storage(dtype: str, compute_shape, halo=(0, 0, 0),
                       strides=strides, view=view, _base=base)
     st._pinned_owner = owner  # keep the allocation alive with the storage
     return st
+
+
+def read_gtsf(source, layout: Optional[LayoutSpec] = None) -> DeviceFieldStorage:
+    """GTSF file -> device storage (the reference reader, storage.py:250-280,
+    then one upload); the b200 layout unless ``layout`` says otherwise."""
+    host = sf_storage.read_gtsf(source, layout or B200_LAYOUT)
+    return to_device(host)
+
+
+def write_gtsf(storage: FieldStorage, sink) -> None:
+    """Device (or host) storage -> GTSF file, bit-exact (storage.py:230-247);
+    a device storage is read back once through its host mirror."""
+    sf_storage.write_gtsf(storage, sink)
