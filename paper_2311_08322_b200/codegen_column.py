@@ -234,8 +234,9 @@ class _Ctx(_MemCtx):
         if self.phase == "f" and name in self.pro_vals and off == (0, 0, 0):
             return self.pro_vals[name]
         if self.phase == "f" and self.ring and name in self.sp.streamed:
-            return (f"((double)((const {self.ctype[name]}*)(sb + {self.offs[name]}))"
-                    f"[(kk * {self.rows} + warp) * {TJ} + lane])")
+            # ur_<f>: this thread's element of level 0 of the stage (hoisted
+            # per stage), so each level is an immediate-offset shared load
+            return f"((double)ur_{name}[kk * {self.rows * TJ}])"
         direction = 1 if self.phase == "f" else -1
         if name in self.cached and not (off[0] or off[1]):
             if off[2] == 0:
@@ -545,9 +546,7 @@ def _emit_variant(kname, plan, sp: ThomasSpec, v: Variant, ctype, dtypes, opts):
         if ring:
             def rd(name, di, dj):
                 hb = v.hbox[name]
-                return (f"((const {ctype[name]}*)(sb + {v.offs[name]}))"
-                        f"[(kk * {rows + hb.rows_extra} + (warp + {di - hb.lo_i})) * {hb.cols}"
-                        f" + (lane + {dj - hb.bstart})]")
+                return f"uh_{name}[kk * {(rows + hb.rows_extra) * hb.cols} + {di * hb.cols + dj}]"
         else:
             def rd(name, di, dj):
                 ii = f"(ic{di:+d})" if di else "ic"
@@ -652,6 +651,11 @@ def _emit_variant(kname, plan, sp: ThomasSpec, v: Variant, ctype, dtypes, opts):
     w("        const uint32_t ph = (uint32_t)(it / NST) & 1u;")
     w("        gts_mbar_wait(&full[s], ph);")
     w("        const unsigned char* sb = smem + s * STB;")
+    for f in sp.streamed:
+        w(f"        const {ctype[f]}* const ur_{f} = (const {ctype[f]}*)(sb + {v.offs[f]}) + warp * {TJ} + lane;")
+    for f, hbx in v.hbox.items():
+        w(f"        const {ctype[f]}* const uh_{f} = (const {ctype[f]}*)(sb + {v.offs[f]})"
+          f" + (warp - ({hbx.lo_i})) * {hbx.cols} + (lane - ({hbx.bstart}));")
     w(f"        const int kbase = kb * {KB};")
     w(f"        const bool fullst = kbase + {KB} <= nk;")
     ctx_f = _Ctx(dtypes, sp, "f", cached_f, ctype)

@@ -300,7 +300,9 @@ def emit(kname: str, plan, kplan, ctype: dict, dtypes: dict, opts=None):
     w(f"// fused PARALLEL tile kernel: {TI}x{TJ} tile per k-plane, {NW} warps x {RI} rows, "
       f"{VJ} columns/lane; streamed {[s.name for s in streams]}, register windows "
       f"{[(x.name, x.rlo, x.rhi, x.clo, x.chi) for x in regw]}")
-    w(f"__global__ void __launch_bounds__({32 * NW}) {kname}(const __grid_constant__ GtsParams p, {tm}, "
+    minb = int((opts or {}).get("pf_minb", 0))  # min resident CTAs/SM (register cap), 0 = compiler's choice
+    lb = f"{32 * NW}, {minb}" if minb else f"{32 * NW}"
+    w(f"__global__ void __launch_bounds__({lb}) {kname}(const __grid_constant__ GtsParams p, {tm}, "
       "int k0, int nkr, int tiles_i, int tiles_j, int ntiles) {")
     w("  extern __shared__ __align__(1024) unsigned char smem[];")
     w(f"  uint64_t* full = (uint64_t*)(smem + {bar_off});")
