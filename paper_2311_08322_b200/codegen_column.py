@@ -63,6 +63,7 @@ class ThomasSpec:
     pro: Optional[object] = None  # codegen_prologue.PrologueSpec fused in front of the forward sweep
     halo: dict = field(default_factory=dict)  # prologue input -> HaloBox
     coop: bool = True  # materialize multi-offset prologue temps cooperatively in smem
+    deep_ring: bool = True  # also instantiate the deeper-ring W=2 geometry
 
 
 @dataclass
@@ -335,7 +336,15 @@ def variants(sp: ThomasSpec, dtypes: dict) -> list:
     esize = {f: (8 if dtypes[f] == ir.F64 else 4) for f in sp.streamed}
     hist_bytes = 4 * sp.w_level  # bytes per level per column
     out = []
-    for w, kb, budget in ((2, 4, 128 * 1024), (1, 8, RING_BUDGET)):
+    # deeper-ring W=2 geometry first: its smaller history tier serves nk <= 80
+    # (the benchmark depth), and the extra stages keep HBM busy while the
+    # backward sweeps run; the regular W=2 and the W=1 geometry cover deeper
+    # columns
+    seen = set()
+    geoms = ((2, 4, 160 * 1024), (2, 4, 128 * 1024), (1, 8, RING_BUDGET))
+    if not sp.deep_ring:
+        geoms = geoms[1:]
+    for w, kb, budget in geoms:
         rows = 4 * w
         offs, sb = {}, 0
         for f in sp.streamed:
@@ -370,10 +379,17 @@ def variants(sp: ThomasSpec, dtypes: dict) -> list:
         hist_off = ring + 2 * half
         smem = ring + 2 * half + sl * nct * hist_bytes + bars + 16
         tl = (512 // w) // sp.w_level
-        if nst * sb > budget:
+        if nst * sb > budget or (w, nst) in seen:
             continue
+        seen.add((w, nst))
         out.append(Variant(w, kb, nst, sb, offs, tl, sl, smem, hist_off, hboxes, tx, mat, ring, half))
     return out
+
+
+def _base_nst(sp, v, dtypes) -> int:
+    """Ring depth of the regular geometry of width v.w (kernel naming)."""
+    budget = 128 * 1024 if v.w == 2 else RING_BUDGET
+    return max(2, min(MAX_STAGES, budget // v.stage_bytes))
 
 
 def emit(kname: str, plan, kplan, sp: ThomasSpec, ctype: dict, dtypes: dict, opts=None,
@@ -386,6 +402,9 @@ def emit(kname: str, plan, kplan, sp: ThomasSpec, ctype: dict, dtypes: dict, opt
     # cooperative materialization measured slower (235 vs 179 us/step: the per-stage
     # consumer barrier serialises the 8 warps), so it is opt-in
     sp.coop = bool((opts or {}).get("pro_coop", False)) and bool((opts or {}).get("pro_batch", True))
+    # measured: the deeper ring helps the fused dycore kernel (181 -> 177 us/step)
+    # and costs vadv ~0.9 us at 256^2, so it defaults on with a prologue only
+    sp.deep_ring = bool((opts or {}).get("deep_ring", sp.pro is not None))
     for v in variants(sp, dtypes):
         if only_w and v.w != int(only_w):
             continue
@@ -394,7 +413,7 @@ def emit(kname: str, plan, kplan, sp: ThomasSpec, ctype: dict, dtypes: dict, opt
         launch_variants.append((cond, call, v))
     launch = ["  {"]
     for f in list(sp.streamed) + list(sp.halo):
-        launch.append(f"    CUtensorMap tm_{f}[2];")
+        launch.append(f"    CUtensorMap tm_{f}[{max(1, len(launch_variants))}];")
     launch.append("    bool launched = false;")
     for vi, (cond, call, v) in enumerate(launch_variants):
         launch.append(f"    if (!launched && nk <= {v.tl + v.sl}) {{")
@@ -444,7 +463,7 @@ def _emit_variant(kname, plan, sp: ThomasSpec, v: Variant, ctype, dtypes, opts):
     ncw = 4 * v.w
     nct = 32 * ncw
     threads = nct + 32
-    kn = f"{kname}_tmem_w{v.w}"
+    kn = f"{kname}_tmem_w{v.w}" + (f"s{v.nst}" if v.nst != _base_nst(sp, v, dtypes) else "")
     wl = sp.w_level
     hb = 4 * wl
     hoff, o = {}, 0
@@ -880,8 +899,8 @@ def _emit_variant(kname, plan, sp: ThomasSpec, v: Variant, ctype, dtypes, opts):
             f"const int tiles_j = (int)((nj + {TJ - 1}) / {TJ});",
             f"const int ntiles = tiles_j * (int)((ni + {rows - 1}) / {rows});",
             "int grid = gts_sm_count(); if (grid > ntiles) grid = ntiles;",
-            f"static bool attr_w{v.w} = false;",
-            f"if (!attr_w{v.w}) {{ cudaFuncSetAttribute({kn}, cudaFuncAttributeMaxDynamicSharedMemorySize, {v.smem_bytes}); attr_w{v.w} = true; }}",
+            f"static bool attr_{kn} = false;",
+            f"if (!attr_{kn}) {{ cudaFuncSetAttribute({kn}, cudaFuncAttributeMaxDynamicSharedMemorySize, {v.smem_bytes}); attr_{kn} = true; }}",
             f"gts_launch_pdl({kn}, dim3(grid), dim3({threads}), {v.smem_bytes}, st, p, {tm_args}, tiles_j, ntiles);",
         ]
 
