@@ -156,6 +156,111 @@ def emit_expr(e, ctx: _Ctx) -> str:
 
 
 # ---------------------------------------------------------------------------
+# binary32-exact emission (f32 storage).  The reference evaluates f32 programs
+# in binary64 and narrows every store; each narrowing and each
+# widening is a 64-bit conversion, which is what bounds an f32 stencil on B200.
+# Three rewrites give the same bits with binary32 instructions:
+#  * a value that is exactly a binary32 number (an f32 field or temporary, a
+#    literal representable in binary32, its negation) is used as a float;
+#  * round_to_f32(x op y), op one of + - * / on binary32-exact x, y and
+#    evaluated in binary64, equals the binary32 operation x op y: binary64
+#    carries 53 >= 2*24 + 2 significand bits and a wider exponent range, so
+#    the double rounding is innocuous (Figueroa, "When is double rounding
+#    innocuous?", SIGNUM 1995; the asm.js Math.fround argument);
+#  * comparisons of two binary32-exact values compare the floats (widening
+#    is exact and monotone), and the flux-limiter sign test
+#    (x0 - y0) * (x1 - y1) > 0 (or < 0) becomes float comparisons: a nonzero
+#    finite difference of binary32 values lies in [2^-149, 2^129], so the
+#    binary64 product neither underflows nor overflows and its sign is the
+#    product of the signs; NaN / inf * 0 cases make both forms false.
+# Contexts opt in with read_f32(); binary64 programs never take these paths.
+# ---------------------------------------------------------------------------
+_ARITH = ("+", "-", "*", "/")
+_CMP = ("<", ">", "<=", ">=", "==", "!=")
+
+
+def _f32_exact_literal(value) -> bool:
+    import struct
+
+    v = float(value)
+    if not math.isfinite(v):
+        return False
+    try:
+        return struct.unpack("f", struct.pack("f", v))[0] == v
+    except OverflowError:
+        return False
+
+
+def emit_f32(e, ctx) -> Optional[str]:
+    """Float spelling of ``e`` when its value is exactly a binary32 number."""
+    rd = getattr(ctx, "read_f32", None)
+    if rd is None:
+        return None
+    if isinstance(e, ir.Literal) and not isinstance(e.value, bool) and _f32_exact_literal(e.value):
+        return float(e.value).hex() + "f"
+    if isinstance(e, ir.FieldAccess):
+        return rd(e.field, e.offset)
+    if isinstance(e, ir.UnaryOp) and e.op == "-":
+        inner = emit_f32(e.operand, ctx)
+        return None if inner is None else f"(-{inner})"
+    return None
+
+
+def emit_f32_rounded(e, ctx) -> Optional[str]:
+    """Float spelling of round_to_binary32(e evaluated in binary64), when one
+    binary32 instruction provably gives it (see above); else None."""
+    v = emit_f32(e, ctx)
+    if v is not None:
+        return v
+    if isinstance(e, ir.BinaryOp) and e.op in _ARITH:
+        a, b = emit_f32(e.left, ctx), emit_f32(e.right, ctx)
+        if a is not None and b is not None:
+            return f"({a} {e.op} {b})"
+    return None
+
+
+def _sign_parts(e, ctx):
+    """(positive, negative) float conditions of a binary64 value that is one
+    +/- of two binary32-exact operands, or binary32-exact itself."""
+    v = emit_f32(e, ctx)
+    if v is not None:
+        return f"({v} > 0.0f)", f"({v} < 0.0f)"
+    if isinstance(e, ir.BinaryOp) and e.op in ("-", "+"):
+        a, b = emit_f32(e.left, ctx), emit_f32(e.right, ctx)
+        if a is not None and b is not None:
+            if e.op == "+":
+                b = f"(-{b})"
+            return f"({a} > {b})", f"({a} < {b})"
+    return None
+
+
+def emit_cond(e, ctx) -> str:
+    """A condition, with the binary32 rewrites where they are exact."""
+    if getattr(ctx, "read_f32", None) is not None and isinstance(e, ir.BinaryOp):
+        if e.op in ("and", "or"):
+            op = _BINOP[e.op]
+            return f"({emit_cond(e.left, ctx)} {op} {emit_cond(e.right, ctx)})"
+        if e.op in _CMP:
+            a, b = emit_f32(e.left, ctx), emit_f32(e.right, ctx)
+            if a is not None and b is not None:
+                return f"({a} {e.op} {b})"
+            if e.op in ("<", ">"):
+                prod, zero_right = None, None
+                if isinstance(e.right, ir.Literal) and float(e.right.value) == 0.0:
+                    prod, zero_right = e.left, True
+                elif isinstance(e.left, ir.Literal) and float(e.left.value) == 0.0:
+                    prod, zero_right = e.right, False
+                if isinstance(prod, ir.BinaryOp) and prod.op == "*":
+                    s1, s2 = _sign_parts(prod.left, ctx), _sign_parts(prod.right, ctx)
+                    if s1 is not None and s2 is not None:
+                        want_pos = (e.op == ">") == zero_right  # P > 0  or  0 < P
+                        if want_pos:
+                            return f"(({s1[0]} && {s2[0]}) || ({s1[1]} && {s2[1]}))"
+                        return f"(({s1[0]} && {s2[1]}) || ({s1[1]} && {s2[0]}))"
+    return emit_expr(e, ctx)
+
+
+# ---------------------------------------------------------------------------
 # Statement emission for memory-backed kernels (pstage / plane / column)
 # ---------------------------------------------------------------------------
 

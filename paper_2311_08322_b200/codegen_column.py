@@ -230,6 +230,7 @@ class _Ctx(_MemCtx):
         return f"GTS_AT(p.f_{name}, {ii}, {jj}, {kk})"
 
     pro_vals: dict = {}
+    kstride = None  # level stride of a ring stage (default rows * TJ)
 
     def read(self, name, off):
         if self.phase == "f" and name in self.pro_vals and off == (0, 0, 0):
@@ -237,7 +238,7 @@ class _Ctx(_MemCtx):
         if self.phase == "f" and self.ring and name in self.sp.streamed:
             # ur_<f>: this thread's element of level 0 of the stage (hoisted
             # per stage), so each level is an immediate-offset shared load
-            return f"((double)ur_{name}[kk * {self.rows * TJ}])"
+            return f"((double)ur_{name}[kk * {self.kstride or self.rows * TJ}])"
         direction = 1 if self.phase == "f" else -1
         if name in self.cached and not (off[0] or off[1]):
             if off[2] == 0:
@@ -475,12 +476,21 @@ def _emit_variant(kname, plan, sp: ThomasSpec, v: Variant, ctype, dtypes, opts):
     out: list = []
     w = out.append
     tm_fields = list(sp.streamed) + list(sp.halo)
+    # two-height tile plan (gts_col_split): the last rounds' tiles are h2 < rows
+    # i-rows high so every SM carries a similar load; streamed-only kernels.
+    # Measured (tools/ksweep.py, B200): 444x256x80 69.2 -> 67.7 us and
+    # 148x256x80 32.6 -> 31.1 us, but 256^2x80 38.2 -> 38.6 us (its second
+    # round is bandwidth-bound either way) and +1% where no split applies
+    # (the runtime level stride), so it is opt-in
+    split = not v.hbox and not v.mat and bool((opts or {}).get("col_split", False))
     tm_params = ", ".join(f"const __grid_constant__ CUtensorMap tm_{f}" for f in tm_fields)
+    if split:
+        tm_params += ", " + ", ".join(f"const __grid_constant__ CUtensorMap tm2_{f}" for f in tm_fields)
     w(f"// TMEM column kernel, W={v.w}: {nct} columns/CTA, streamed {sp.streamed} (ring {v.nst} x"
       f" {v.stage_bytes} B), history {sp.cross}: TMEM levels [0,{v.tl}), smem levels"
       f" [{v.tl},{v.tl + v.sl})")
     w(f"__global__ void __launch_bounds__({threads}, 1) {kn}(const __grid_constant__ GtsParams p, "
-      f"{tm_params}, int tiles_j, int ntiles) {{")
+      f"{tm_params}, int tiles_j, int ntiles" + (", int n1, int isplit, int h2" if split else "") + ") {")
     w("  extern __shared__ __align__(1024) unsigned char smem[];")
     w(f"  constexpr int NST = {v.nst};")
     w(f"  constexpr unsigned STB = {v.stage_bytes}u;")
@@ -509,14 +519,31 @@ def _emit_variant(kname, plan, sp: ThomasSpec, v: Variant, ctype, dtypes, opts):
         w(f"      gts_prefetch_tensormap(&tm_{f});")
     w("      int it = 0;")
     w("      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {")
-    w(f"        const int j0 = (t % tiles_j) * {TJ}, i0 = (t / tiles_j) * {rows};")
+    if split:
+        assert v.tx % rows == 0
+        w("        const bool c2_ = t >= n1;")
+        w("        const int u_ = c2_ ? t - n1 : t;")
+        w(f"        const int j0 = (u_ % tiles_j) * {TJ}, i0 = c2_ ? isplit + (u_ / tiles_j) * h2 : (u_ / tiles_j) * {rows};")
+        w(f"        const uint32_t txb_ = c2_ ? (uint32_t)h2 * {v.tx // rows}u : {v.tx}u;")
+    else:
+        w(f"        const int j0 = (t % tiles_j) * {TJ}, i0 = (t / tiles_j) * {rows};")
     w("        for (int kb = 0; kb < nkb; ++kb, ++it) {")
     w("          const int s = it % NST;")
     w("          const uint32_t ph = (uint32_t)(it / NST) & 1u;")
     w("          if (it >= NST) gts_mbar_wait_sleep(&empty[s], ph ^ 1u);")
-    w(f"          gts_mbar_arrive_expect_tx(&full[s], {v.tx}u);")
-    for f in tm_fields:
-        w(f"          gts_tma_load_3d(smem + s * STB + {v.offs[f]}, &tm_{f}, &full[s], j0, i0, kb * {KB});")
+    if split:
+        w("          gts_mbar_arrive_expect_tx(&full[s], txb_);")
+        w("          if (c2_) {")
+        for f in tm_fields:
+            w(f"            gts_tma_load_3d(smem + s * STB + {v.offs[f]}, &tm2_{f}, &full[s], j0, i0, kb * {KB});")
+        w("          } else {")
+        for f in tm_fields:
+            w(f"            gts_tma_load_3d(smem + s * STB + {v.offs[f]}, &tm_{f}, &full[s], j0, i0, kb * {KB});")
+        w("          }")
+    else:
+        w(f"          gts_mbar_arrive_expect_tx(&full[s], {v.tx}u);")
+        for f in tm_fields:
+            w(f"          gts_tma_load_3d(smem + s * STB + {v.offs[f]}, &tm_{f}, &full[s], j0, i0, kb * {KB});")
     w("        }")
     w("      }")
     w("    }")
@@ -531,7 +558,22 @@ def _emit_variant(kname, plan, sp: ThomasSpec, v: Variant, ctype, dtypes, opts):
     for gi, (iv, _) in enumerate(gb):
         w(f"    const int b{gi}k0 = {_bound(iv.start)}, b{gi}k1 = {_bound(iv.end)};")
     w("    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {")
-    w(f"      const int j = (t % tiles_j) * {TJ} + lane, i = (t / tiles_j) * {rows} + warp;")
+    if split:
+        w("      const bool c2_ = t >= n1;")
+        w("      const int u_ = c2_ ? t - n1 : t;")
+        w(f"      const int h_ = c2_ ? h2 : {rows};")
+        w(f"      const int hs_ = h_ * {TJ};  // level stride of a ring stage's boxes")
+        w(f"      const int j = (u_ % tiles_j) * {TJ} + lane, i = (c2_ ? isplit + (u_ / tiles_j) * h2 : (u_ / tiles_j) * {rows}) + warp;")
+        w("      if (warp >= h_ || i >= p.ni) {  // no row of this tile: keep the ring's phases only")
+        w("        for (int kb = 0; kb < nkb; ++kb, ++it) {")
+        w("          gts_mbar_wait(&full[it % NST], (uint32_t)(it / NST) & 1u);")
+        w("          __syncwarp();")
+        w("          if (lane == 0) gts_mbar_arrive(&empty[it % NST]);")
+        w("        }")
+        w("        continue;")
+        w("      }")
+    else:
+        w(f"      const int j = (t % tiles_j) * {TJ} + lane, i = (t / tiles_j) * {rows} + warp;")
     w("      const bool valid = (i < p.ni) && (j < p.nj);")
     w("      const int ic = i < p.ni ? i : p.ni - 1, jc = j < p.nj ? j : p.nj - 1;")
     w("      (void)ic; (void)jc;")
@@ -679,6 +721,7 @@ def _emit_variant(kname, plan, sp: ThomasSpec, v: Variant, ctype, dtypes, opts):
     w(f"        const bool fullst = kbase + {KB} <= nk;")
     ctx_f = _Ctx(dtypes, sp, "f", cached_f, ctype)
     ctx_f.rows, ctx_f.kb, ctx_f.offs = rows, KB, v.offs
+    ctx_f.kstride = "hs_" if split else str(rows * TJ)
     first = True
     for tier, tcond in (("tmem", "kbase < TL"), ("smem", "kbase >= TL")):
         for gi in range(len(gf)):
@@ -895,14 +938,35 @@ def _emit_variant(kname, plan, sp: ThomasSpec, v: Variant, ctype, dtypes, opts):
 
     def call(vi):
         tm_args = ", ".join(f"tm_{f}[{vi}]" for f in tm_fields)
-        return [
+        if not split:
+            return [
+                f"const int tiles_j = (int)((nj + {TJ - 1}) / {TJ});",
+                f"const int ntiles = tiles_j * (int)((ni + {rows - 1}) / {rows});",
+                "int grid = gts_sm_count(); if (grid > ntiles) grid = ntiles;",
+                f"static bool attr_{kn} = false;",
+                f"if (!attr_{kn}) {{ cudaFuncSetAttribute({kn}, cudaFuncAttributeMaxDynamicSharedMemorySize, {v.smem_bytes}); attr_{kn} = true; }}",
+                f"gts_launch_pdl({kn}, dim3(grid), dim3({threads}), {v.smem_bytes}, st, p, {tm_args}, tiles_j, ntiles);",
+            ]
+        lines = [
             f"const int tiles_j = (int)((nj + {TJ - 1}) / {TJ});",
-            f"const int ntiles = tiles_j * (int)((ni + {rows - 1}) / {rows});",
-            "int grid = gts_sm_count(); if (grid > ntiles) grid = ntiles;",
+            f"GtsColSplit cs_ = gts_col_split((int)ni, (int)nj, {rows}, gts_sm_count());",
+        ]
+        for f in tm_fields:
+            e = 8 if dtypes[f] == ir.F64 else 4
+            lines.append(f"CUtensorMap tm2_{f} = tm_{f}[{vi}];")
+            lines.append(
+                f"if (cs_.h2 > 0 && !gts_make_tmap_3d(&tm2_{f}, (const void*)p.f_{f}.p, {e}, nj, ni, nk,"
+                f" p.f_{f}.si, p.f_{f}.sj, p.f_{f}.sk, {TJ}, (unsigned)cs_.h2, {v.kb}))"
+                f" cs_ = {{tiles_j * (int)((ni + {rows - 1}) / {rows}), 0, 0, tiles_j * (int)((ni + {rows - 1}) / {rows})}};")
+        tm2_args = ", ".join(f"tm2_{f}" for f in tm_fields)
+        lines += [
+            "int grid = gts_sm_count(); if (grid > cs_.ntiles) grid = cs_.ntiles;",
             f"static bool attr_{kn} = false;",
             f"if (!attr_{kn}) {{ cudaFuncSetAttribute({kn}, cudaFuncAttributeMaxDynamicSharedMemorySize, {v.smem_bytes}); attr_{kn} = true; }}",
-            f"gts_launch_pdl({kn}, dim3(grid), dim3({threads}), {v.smem_bytes}, st, p, {tm_args}, tiles_j, ntiles);",
+            f"gts_launch_pdl({kn}, dim3(grid), dim3({threads}), {v.smem_bytes}, st, p, {tm_args}, {tm2_args},"
+            " tiles_j, cs_.ntiles, cs_.n1, cs_.isplit, cs_.h2 > 0 ? cs_.h2 : 1);",
         ]
+        return lines
 
     return out, None, call
 

@@ -30,7 +30,7 @@ from __future__ import annotations
 from dataclasses import dataclass, field
 
 from ._host import ir
-from .codegen import DivPool, _bound, c_float, emit_expr  # noqa: F401
+from .codegen import DivPool, _bound, c_float, emit_cond, emit_expr, emit_f32_rounded  # noqa: F401
 from .lowering import always_writes, reads, writes
 
 NW = 4  # warps per CTA
@@ -195,6 +195,19 @@ class _Ctx:
     def __init__(self, geo: Geo, ctype: dict, stage_hi: int, col: int):
         self.geo, self.ctype, self.hi, self.col = geo, ctype, stage_hi, col
 
+    f32x = True  # binary32-exact rewrites for f32 storage (codegen.emit_f32)
+
+    def read_f32(self, name, off):
+        """Float spelling of an f32 field / temporary (None: not binary32)."""
+        if not self.f32x or self.ctype.get(name) != "float":
+            return None
+        di, dj, dk = off
+        wv = self.geo.wins.get(name)
+        if wv is not None and dk == 0:
+            row = _phys(self.geo, wv, self.hi + di - wv.rlo)
+            return f"wf_{name}[{row}][{self.col + dj - wv.clo}]"
+        return f"GTS_AT(p.f_{name}, (r + {self.hi + di}), (jl + {self.col + dj}), (kk + {dk}))"
+
     def read(self, name, off):
         di, dj, dk = off
         wv = self.geo.wins.get(name)
@@ -214,28 +227,45 @@ def _emit_point(stmt, ctx: _Ctx, ctype, api: set, out: list, indent: str, local:
     pool = ctx.pool
     if isinstance(stmt, ir.Assign):
         name = stmt.target.field
-        value = emit_expr(stmt.value, ctx)
-        pool.flush(indent, out)
-        out.append(f"{indent}{{ const double v_ = {value};")
+        f32 = ctx.f32x and ctype[name] == "float"
+        fv = emit_f32_rounded(stmt.value, ctx) if f32 else None
+        if fv is not None:
+            # one binary32 instruction gives the narrowed value exactly
+            pool.flush(indent, out)
+            out.append(f"{indent}{{ const float vf_ = {fv};")
+            sv = "vf_"
+        else:
+            value = emit_expr(stmt.value, ctx)
+            pool.flush(indent, out)
+            out.append(f"{indent}{{ const double v_ = {value};")
+            if f32:
+                out.append(f"{indent}  const float vf_ = (float)v_;")
+                sv = "vf_"
+            else:
+                sv = f"({ctype[name]})(v_)"
         wv = geo.wins.get(name)
         if wv is not None and wv.kind in ("temp", "own"):
             row = _phys(geo, wv, ctx.hi - wv.rlo)
             c = ctx.col - wv.clo
-            out.append(f"{indent}  w_{name}[{row}][{c}] = (double)({ctype[name]})(v_);")
+            if f32:
+                out.append(f"{indent}  wf_{name}[{row}][{c}] = vf_;")
+                out.append(f"{indent}  w_{name}[{row}][{c}] = (double)vf_;")
+            else:
+                out.append(f"{indent}  w_{name}[{row}][{c}] = (double)({ctype[name]})(v_);")
         if name in api and name in geo.buffered:
-            out.append(f"{indent}  o_{name}[{ctx.col}] = ({ctype[name]})(v_);")
+            out.append(f"{indent}  o_{name}[{ctx.col}] = {sv};")
         elif name in api:
-            out.append(f"{indent}  if (ok_{_cn(ctx.col)}) GTS_AT(p.f_{name}, r, (jl + {ctx.col}), kk) = ({ctype[name]})(v_);")
+            out.append(f"{indent}  if (ok_{_cn(ctx.col)}) GTS_AT(p.f_{name}, r, (jl + {ctx.col}), kk) = {sv};")
         elif name in ctx.arena:
             # arena copy for later launches: every point of the stage's extent
             li, hi, lj, hj = ctx.stage_ext
             out.append(f"{indent}  if ((r + {hi}) < ni + {hi} && (jl + {ctx.col}) >= {lj} && (jl + {ctx.col}) < nj + {hj})"
-                       f" GTS_AT(p.f_{name}, (r + {hi}), (jl + {ctx.col}), kk) = ({ctype[name]})(v_);")
+                       f" GTS_AT(p.f_{name}, (r + {hi}), (jl + {ctx.col}), kk) = {sv};")
         out.append(f"{indent}}}")
         pool.invalidate(name)
         return
     if isinstance(stmt, ir.If):
-        cond = emit_expr(stmt.cond, ctx)
+        cond = emit_cond(stmt.cond, ctx)
         pool.flush(indent, out)
         out.append(f"{indent}if ({cond}) {{")
         pool.depth += 1
@@ -361,13 +391,18 @@ def emit(kname: str, plan, kplan, ctype: dict, dtypes: dict, opts=None):
     for c in range(VJ):
         w(f"    const bool okc_{c} = (jl + {c}) < nj;")
     # register windows
+    f32x = bool((opts or {}).get("f32x", True))
     for x in regw:
         w(f"    double w_{x.name}[{x.rhi - x.rlo + 1}][{x.chi - x.clo + 1}];")
+        if f32x and ctype[x.name] == "float":
+            w(f"    float wf_{x.name}[{x.rhi - x.rlo + 1}][{x.chi - x.clo + 1}];")
     # stream windows are read from smem directly: define accessor macros
     for s in streams:
         row_base = geo.min_step + s.rlo  # smem row 0 <-> absolute row i0 + row_base
         w(f"    const {ctype[s.name]}* const sp_{s.name} = (const {ctype[s.name]}*)(sb + {s.smem_off});")
         w(f"    double w_{s.name}[{s.rhi - s.rlo + 1}][{s.chi - s.clo + 1}];")
+        if f32x and ctype[s.name] == "float":
+            w(f"    float wf_{s.name}[{s.rhi - s.rlo + 1}][{s.chi - s.clo + 1}];")
     steps_lo = geo.min_step
     nsteps = RI - steps_lo  # steps r = ra + min_step .. ra + RI - 1
 
@@ -385,14 +420,19 @@ def emit(kname: str, plan, kplan, ctype: dict, dtypes: dict, opts=None):
                 v //= 2
             idx = f"{rowexpr} + lane * {VJ} + {off + c}"
             prow = _phys(geo, s, rowidx)
+            fl = f32x and s.esize == 4
             if v == 1:
                 w(f"      w_{s.name}[{prow}][{c}] = (double)sp_{s.name}[{idx}];")
+                if fl:
+                    w(f"      wf_{s.name}[{prow}][{c}] = sp_{s.name}[{idx}];")
             else:
                 vt = {(8, 2): "double2", (4, 2): "float2", (4, 4): "float4"}[(s.esize, v)]
                 w(f"      {{ const {vt} q_ = *reinterpret_cast<const {vt}*>(sp_{s.name} + {idx});")
                 comps = "xyzw"
                 for q in range(v):
                     w(f"        w_{s.name}[{prow}][{c + q}] = (double)q_.{comps[q]};")
+                    if fl:
+                        w(f"        wf_{s.name}[{prow}][{c + q}] = q_.{comps[q]};")
                 w("      }")
             c += v
 
@@ -420,6 +460,7 @@ def emit(kname: str, plan, kplan, ctype: dict, dtypes: dict, opts=None):
             w(f"      {{ // stage {si} at row r + {hi}")
             for col in range(lj, VJ + hj):
                 ctx = _Ctx(geo, ctype, hi, col)
+                ctx.f32x = f32x
                 ctx.pool = DivPool("branch")
                 ctx.arena = set(plan.global_temps)
                 ctx.stage_ext = geo.ext[si]
@@ -430,6 +471,8 @@ def emit(kname: str, plan, kplan, ctype: dict, dtypes: dict, opts=None):
                         # a conditionally written temporary reads as NaN where
                         # unwritten, like the reference's NaN-initialised ones
                         w(f"          w_{f}[{_phys(geo, wv, hi - wv.rlo)}][{col - wv.clo}] = GTS_NAN;")
+                        if f32x and ctype[f] == "float":
+                            w(f"          wf_{f}[{_phys(geo, wv, hi - wv.rlo)}][{col - wv.clo}] = __int_as_float(0x7fffffff);")
                 _emit_point(st.body, ctx, ctype, api, out, "          ", local, geo)
                 w("        }")
             w("      }")

@@ -6,6 +6,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <vector>
 
 // ---------------------------------------------------------------------------
 // mbarrier
@@ -261,4 +262,64 @@ static int gts_sm_count() {
     if (n <= 0) n = 148;
   }
   return n;
+}
+
+// ---------------------------------------------------------------------------
+// Two-height tile plan of the persistent column kernels.  Tiles are `rows`
+// i-rows x 32 j-columns; CTA b of a grid of G takes tiles b, b+G, ...  When
+// the tile count is not a multiple of G, the last round leaves SMs idle while
+// the others run a whole extra tile (256^2 x 80 vadv: 256 tiles on 148 SMs).
+// The plan covers i in [0, isplit) with rows-high tiles (the first n1 tiles)
+// and i in [isplit, ni) with h2-high tiles, chosen to minimise the most
+// loaded SM.  Cost of an h-row tile ~ max(h, 0.72 rows): measured on B200, a
+// lone 8-row tile runs in ~13 us (its serial recurrence) against ~18 us per
+// bandwidth-bound round of 8-row tiles (tools/ksweep.py).
+// ---------------------------------------------------------------------------
+struct GtsColSplit {
+  int n1, isplit, h2, ntiles;
+};
+
+static long gts_col_split_cost(int ni, int tj, int rows, int isplit, int h2, int G) {
+  static thread_local std::vector<long> load;
+  load.assign((size_t)G, 0);
+  const long lat = (72L * rows + 99) / 100;
+  long t = 0, worst = 0;
+  auto add = [&](int h, int count) {
+    const long c = (h > lat ? h : lat);
+    for (int q = 0; q < count; ++q, ++t) {
+      long& l = load[(size_t)(t % G)];
+      l += c;
+      if (l > worst) worst = l;
+    }
+  };
+  for (int i0 = 0; i0 < isplit; i0 += rows) add(i0 + rows <= ni ? rows : ni - i0, tj);
+  if (h2 > 0)
+    for (int i0 = isplit; i0 < ni; i0 += h2) add(i0 + h2 <= ni ? h2 : ni - i0, tj);
+  return worst;
+}
+
+static GtsColSplit gts_col_split(int ni, int nj, int rows, int G) {
+  static thread_local int cni = -1, cnj = -1, crows = -1, cG = -1;
+  static thread_local GtsColSplit cached;
+  if (ni == cni && nj == cnj && rows == crows && G == cG) return cached;
+  const int tj = (nj + 31) / 32;
+  const int full = (ni + rows - 1) / rows;
+  GtsColSplit best = {full * tj, full * rows, 0, full * tj};
+  if ((long)full * tj > G && ((long)full * tj) % G != 0) {
+    long bc = gts_col_split_cost(ni, tj, rows, full * rows, 0, G);
+    // the h2 tiles only ever need to cover the last ~2 rounds
+    // (largest isplit first: at equal cost, keep more full-height tiles)
+    const int span = 2 * ((G + tj - 1) / tj) * rows + rows;
+    const int is_lo = full * rows - span > 0 ? ((full * rows - span) / rows) * rows : 0;
+    for (int is = ((ni - 1) / rows) * rows; is >= is_lo; is -= rows)
+      for (int h2 = rows - 1; h2 >= 1; --h2) {
+        const long c = gts_col_split_cost(ni, tj, rows, is, h2, G);
+        if (c * 50 < bc * 49) {  // > 2% better than the best so far
+          bc = c;
+          best = {(is / rows) * tj, is, h2, (is / rows) * tj + ((ni - is + h2 - 1) / h2) * tj};
+        }
+      }
+  }
+  cni = ni, cnj = nj, crows = rows, cG = G, cached = best;
+  return best;
 }
