@@ -406,6 +406,25 @@ def emit(kname: str, plan, kplan, ctype: dict, dtypes: dict, opts=None):
     steps_lo = geo.min_step
     nsteps = RI - steps_lo  # steps r = ra + min_step .. ra + RI - 1
 
+    # Shared-memory bank spreading: lane l reads VJ consecutive elements, so
+    # with a lane stride S = VJ * esize bytes > the vector width V, lanes l
+    # and l + 128/S hit the same banks in one instruction (f64: 2-way, half
+    # the LDS bandwidth).  Chunks are loaded in pairs whose offsets differ by
+    # V..S-V (mod S): lane groups alternate which one they load first, so one
+    # instruction covers all 32 banks; selects put the values back in place.
+    # Measured (tools/ksweep.py, B200): hdiff f64 256^2x80 17.11 -> 16.77 us,
+    # but 512x1024x80 113.1 -> 116.1 us and f32 256^2 15.65 -> 16.49 us (the
+    # selects cost more than the halved wavefronts save), so it is opt-in.
+    lane_stride = {s.name: VJ * s.esize for s in streams}
+    swz = {}
+    for s in streams:
+        S = lane_stride[s.name]
+        g = 128 // S if S and 128 % S == 0 else 0
+        if bool((opts or {}).get("pf_swz", False)) and g >= 1 and (g & (g - 1)) == 0 and 1 < g <= 16:
+            swz[s.name] = g
+    for g in sorted(set(swz.values())):
+        w(f"    const int swz{g}_ = (lane / {g}) & 1;")
+
     def load_stream_row(s, rowidx, rel_row):
         # absolute row = r + rel_row; smem row = (r + rel_row) - (i0 + min_step + rlo);
         # 8/16-B vector loads where the layout allows (rows are 16-B multiples)
@@ -413,28 +432,68 @@ def emit(kname: str, plan, kplan, ctype: dict, dtypes: dict, opts=None):
         ncol = s.chi - s.clo + 1
         rowexpr = f"(size_t)((r + {rel_row}) - (i0 + {geo.min_step + s.rlo})) * {s.box_cols}"
         vmax = 16 // s.esize
+        chunks = []
         c = 0
         while c < ncol:
             v = vmax
             while v > 1 and not ((off + c) % v == 0 and VJ % v == 0 and c + v <= ncol):
                 v //= 2
+            chunks.append((c, v))
+            c += v
+        prow = _phys(geo, s, rowidx)
+        fl = f32x and s.esize == 4
+        comps = "xyzw"
+        S = lane_stride[s.name]
+
+        def assign(c, v, q):
+            for k in range(v):
+                w(f"        w_{s.name}[{prow}][{c + k}] = (double){q}.{comps[k]};")
+                if fl:
+                    w(f"        wf_{s.name}[{prow}][{c + k}] = {q}.{comps[k]};")
+
+        # pair chunks for bank spreading
+        pairs, used = [], set()
+        if s.name in swz:
+            for a, (ca, va) in enumerate(chunks):
+                if a in used or va == 1 or va * s.esize >= S:
+                    continue
+                V = va * s.esize
+                for b in range(a + 1, len(chunks)):
+                    cb, vb = chunks[b]
+                    if b in used or vb != va:
+                        continue
+                    d = ((cb - ca) * s.esize) % S
+                    if V <= d <= S - V:
+                        pairs.append((a, b))
+                        used |= {a, b}
+                        break
+        partner = {a: b for a, b in pairs}
+        for a, (c, v) in enumerate(chunks):
             idx = f"{rowexpr} + lane * {VJ} + {off + c}"
-            prow = _phys(geo, s, rowidx)
-            fl = f32x and s.esize == 4
-            if v == 1:
+            if v == 1 and a not in used:
                 w(f"      w_{s.name}[{prow}][{c}] = (double)sp_{s.name}[{idx}];")
                 if fl:
                     w(f"      wf_{s.name}[{prow}][{c}] = sp_{s.name}[{idx}];")
-            else:
-                vt = {(8, 2): "double2", (4, 2): "float2", (4, 4): "float4"}[(s.esize, v)]
-                w(f"      {{ const {vt} q_ = *reinterpret_cast<const {vt}*>(sp_{s.name} + {idx});")
-                comps = "xyzw"
-                for q in range(v):
-                    w(f"        w_{s.name}[{prow}][{c + q}] = (double)q_.{comps[q]};")
-                    if fl:
-                        w(f"        wf_{s.name}[{prow}][{c + q}] = q_.{comps[q]};")
+                continue
+            vt = {(8, 2): "double2", (4, 2): "float2", (4, 4): "float4"}[(s.esize, v)]
+            if a in partner:
+                b = partner[a]
+                cb = chunks[b][0]
+                sw = f"swz{swz[s.name]}_"
+                dlt = cb - c
+                w(f"      {{ const {vt} qa_ = *reinterpret_cast<const {vt}*>(sp_{s.name} + {idx} + {sw} * {dlt});")
+                w(f"        const {vt} qb_ = *reinterpret_cast<const {vt}*>(sp_{s.name} + {idx} + (1 - {sw}) * {dlt});")
+                w(f"        const {vt} q0_ = {sw} ? qb_ : qa_;")
+                w(f"        const {vt} q1_ = {sw} ? qa_ : qb_;")
+                assign(c, v, "q0_")
+                assign(cb, v, "q1_")
                 w("      }")
-            c += v
+                continue
+            if a in used:
+                continue  # loaded with its partner
+            w(f"      {{ const {vt} q_ = *reinterpret_cast<const {vt}*>(sp_{s.name} + {idx});")
+            assign(c, v, "q_")
+            w("      }")
 
     # fully unrolled steps (prologue + main)
     for step in range(nsteps):
