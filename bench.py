@@ -470,7 +470,7 @@ def decomposed_hdiff(dist, steps, warmup, tile=(512, 1024, 80)):
     return ms, gdom, grid, step.launches_per_step
 
 
-def dycore_timed(dist, steps=100, domain=(512, 512, 80), reps=3):
+def dycore_timed(dist, steps=100, domain=(512, 512, 80), reps=3, gen_options=None):
     """BASELINE.json configs[4]: the dycore-like step (kernels/dycore.gts:
     hdiff -> Thomas solve -> interval-specialised update) on 512x512x80 f64,
     ``steps`` time steps per run captured in one CUDA graph (TimeLoop); one
@@ -480,7 +480,7 @@ def dycore_timed(dist, steps=100, domain=(512, 512, 80), reps=3):
     from paper_2311_08322_b200 import native, workloads
     from paper_2311_08322_b200.timeloop import TimeLoop
 
-    st = b200.compile_stencil(workloads.source("dycore"), "dycore")
+    st = b200.compile_stencil(workloads.source("dycore"), "dycore", gen_options=gen_options)
     arr = workloads.dycore_arrays(domain, 1000 + dist.rank)
     A, B = b200.from_array(arr["u"], (2, 2, 0)), b200.from_array(arr["u"], (2, 2, 0))
     coef = {n: b200.from_array(arr[n]) for n in "abc"}

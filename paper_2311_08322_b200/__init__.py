@@ -16,7 +16,8 @@ are accepted too (copied to the device around each call).
 from ._host import sf as stencilforge  # noqa: F401  (the reference framework)
 from .api import compile_stencil, install
 from .backend import BACKEND_ID
-from .storage import B200_LAYOUT, DeviceFieldStorage, allocate, from_array, to_device
+from .storage import (B200_LAYOUT, DeviceFieldStorage, ExternalDeviceFieldStorage, allocate, from_array,
+                      from_cuda_array, to_device)
 
 __version__ = "0.1.0"
 
@@ -24,9 +25,11 @@ __all__ = [
     "BACKEND_ID",
     "B200_LAYOUT",
     "DeviceFieldStorage",
+    "ExternalDeviceFieldStorage",
     "allocate",
     "compile_stencil",
     "from_array",
+    "from_cuda_array",
     "install",
     "to_device",
 ]

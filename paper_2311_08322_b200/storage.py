@@ -182,6 +182,73 @@ class DeviceFieldStorage(FieldStorage):
                 f"origin={self.origin}, strides={self.strides}, device={self.device})")
 
 
+class ExternalDeviceFieldStorage(DeviceFieldStorage):
+    """Zero-copy DeviceFieldStorage over a device array owned elsewhere (any
+    object exporting ``__cuda_array_interface__`` v2/v3: a torch.cuda tensor,
+    CuPy, Numba).  The stencil reads and writes the caller's memory in place;
+    ``view`` / ``host_array()`` go through a pinned host mirror like the
+    owning storage.  The array must be 3-D in logical (i, j, k) order with
+    the b200 axis order (k outermost, j contiguous: strides s_k >= s_i >= s_j
+    = 1 element), e.g. ``torch.empty(nk, ni, nj).permute(1, 2, 0)``; any
+    padding is allowed (kernels needing 16-B aligned strides for TMA fall
+    back to their plain form at run time)."""
+
+    def __init__(self, obj, origin=(0, 0, 0)):  # noqa: D107 - documented above
+        cai = getattr(obj, "__cuda_array_interface__", None)
+        if cai is None:
+            raise StorageError(Code.ALLOCATION, f"{type(obj).__name__} has no __cuda_array_interface__")
+        shape = tuple(int(x) for x in cai["shape"])
+        if len(shape) != 3:
+            raise StorageError(Code.ALLOCATION, f"expected a 3-D array, got shape {shape}")
+        dtype = {"<f8": "f64", "<f4": "f32"}.get(np.dtype(cai["typestr"]).str)
+        if dtype is None:
+            raise StorageError(Code.ALLOCATION, f"unsupported element type {cai['typestr']!r}")
+        item = _NP[dtype].itemsize
+        bstrides = cai.get("strides")
+        if bstrides is None:  # C-contiguous
+            bstrides = (shape[1] * shape[2] * item, shape[2] * item, item)
+        if any(b % item or b <= 0 for b in bstrides):
+            raise StorageError(Code.ALLOCATION, f"strides {bstrides} are not positive element multiples")
+        strides = tuple(b // item for b in bstrides)
+        si, sj, sk = strides
+        if not (sj == 1 and si >= shape[1] and sk >= si * shape[0]):
+            raise StorageError(Code.ALLOCATION,
+                               f"strides {strides} (elements, i/j/k) are not the b200 axis order "
+                               "(k outermost, j contiguous)")
+        ptr, _readonly = cai["data"]
+        stream = cai.get("stream")
+        if stream:  # v3: work queued on the producer's stream must finish first
+            native.call("gts_b200_stream_synchronize", int(stream))
+        self.device = native.require_device()
+        self._ext, self._ptr = obj, int(ptr)
+        total = 1 + sum((n - 1) * st for n, st in zip(shape, strides))
+        self._total = total
+        self._host = _PinnedHost(total * item)
+        raw = (ctypes.c_char * (total * item)).from_address(self._host.hptr)
+        host_flat = np.frombuffer(raw, dtype=_NP[dtype])
+        self._host_view = np.lib.stride_tricks.as_strided(
+            host_flat, shape=shape, strides=tuple(x * item for x in strides))
+        self.dtype = dtype
+        self.shape = shape
+        self.origin = tuple(int(x) for x in origin)
+        self.layout = B200_LAYOUT
+        self.strides = strides
+        self._base = host_flat
+        self._host_dirty = False  # the device copy is the authoritative one
+        self._device_dirty = True  # the host mirror has never been filled
+
+    def base_address(self) -> int:
+        return self._ptr
+
+    def _host_span_addr(self) -> int:
+        return self._host.hptr
+
+
+def from_cuda_array(obj, origin=(0, 0, 0)) -> ExternalDeviceFieldStorage:
+    """Wrap a device array (``__cuda_array_interface__``) without copying."""
+    return ExternalDeviceFieldStorage(obj, origin)
+
+
 def allocate(dtype: str, compute_shape, halo=(0, 0, 0), layout: Optional[LayoutSpec] = None,
              fill: Union[str, float] = "zeros") -> DeviceFieldStorage:
     """Device twin of ``stencilforge.allocate`` (storage.py:163-192)."""

@@ -78,3 +78,25 @@ def test_sass_has_no_fma_for_parity_build():
         pytest.skip("cuobjdump unavailable")
     assert "DFMA" not in out.stdout
     assert "DADD" in out.stdout and "DMUL" in out.stdout
+
+
+class _FakeCAI:
+    def __init__(self, shape, strides, typestr="<f8"):
+        self.__cuda_array_interface__ = {"shape": shape, "strides": strides, "typestr": typestr,
+                                         "data": (0x1000, False), "version": 3}
+
+
+@pytest.mark.parametrize("shape,strides,typestr", [
+    ((4, 5), None, "<f8"),                        # not 3-D
+    ((4, 5, 6), None, "<i4"),                     # element type
+    ((4, 5, 6), None, "<f8"),                     # C order: k contiguous, not the b200 axis order
+    ((4, 5, 6), (40, 8, 12), "<f8"),              # strides not element multiples
+    ((4, 5, 6), (48, 8, 160), "<f8"),             # s_k < s_i * ni
+])
+def test_from_cuda_array_rejects_bad_arrays(shape, strides, typestr):
+    """Zero-copy wrapping validates shape / dtype / axis order before touching
+    the device (storage.ExternalDeviceFieldStorage)."""
+    from paper_2311_08322_b200.storage import StorageError
+
+    with pytest.raises(StorageError):
+        b200.from_cuda_array(_FakeCAI(shape, strides, typestr))

@@ -17,7 +17,16 @@ import paper_2311_08322_b200 as b200  # noqa: E402
 from paper_2311_08322_b200 import native, workloads  # noqa: E402
 
 
+def time_dycore(dom, opts):
+    import bench
+
+    r = bench.dycore_timed(bench.Dist(), domain=dom, gen_options=opts or None)
+    return r["ms_per_step"] * 1e3, r["achieved_gbs"], r["plan"]
+
+
 def time_one(kernel, dtype, dom, opts, steps=200, eager=0):
+    if kernel == "dycore":
+        return time_dycore(dom, opts)
     st = b200.compile_stencil(workloads.source(kernel, dtype), kernel, gen_options=opts or None)
     info = native.device_info()
     set_bytes = workloads.algorithmic_bytes(kernel, dom, dtype)
