@@ -78,11 +78,15 @@ class Dist:
         self.rank = int(os.environ.get("RANK", "0"))
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
         self.pg = None
+        # GTS_BENCH_SHARED_GPU=1: all ranks on the box's GPU(s) round-robin, gloo
+        # for the plumbing -- exercises the N>1 code paths on a 1-GPU box (its
+        # numbers are not scaling numbers)
+        self.shared = os.environ.get("GTS_BENCH_SHARED_GPU") == "1"
         if self.world > 1:
             import torch
             import torch.distributed as dist
 
-            backend = "nccl" if torch.cuda.is_available() else "gloo"
+            backend = "nccl" if torch.cuda.is_available() and not self.shared else "gloo"
             if backend == "nccl":
                 torch.cuda.set_device(self.local)
             dist.init_process_group(backend=backend)
@@ -436,7 +440,7 @@ def e2e_timed(st, kernel, dtype, domain, steps):
     return dt, tr["h2d"], tr["d2h"], tr["chunks"]
 
 
-def decomposed_hdiff(dist, steps, warmup, tile=(512, 1024, 80)):
+def decomposed_hdiff(dist, steps, warmup, tile=(512, 1024, 80), transport="nccl"):
     """C4: hdiff on a horizontally decomposed domain, a fixed 512x1024x80
     tile per GPU (weak scaling; 2048x2048x80 at 8 GPUs on a 4x2 grid); each
     step = NCCL halo exchange of inp overlapped with the interior + boundary
@@ -452,7 +456,10 @@ def decomposed_hdiff(dist, steps, warmup, tile=(512, 1024, 80)):
     rng = np.random.default_rng(1000 + dist.rank)
     inp = b200.from_array(rng.uniform(-1, 1, (ldom[0] + 4, ldom[1] + 4, ldom[2])), (2, 2, 0))
     out = b200.allocate("f64", ldom)
-    step = decomp.DecomposedStep(st, d, {"inp": inp, "out": out}, {"coeff": 0.05}, "inp", (2, 2))
+    if transport == "peer":
+        step = decomp.PeerDecomposedStep(st, d, {"inp": inp, "out": out}, {"coeff": 0.05}, "inp", (2, 2))
+    else:
+        step = decomp.DecomposedStep(st, d, {"inp": inp, "out": out}, {"coeff": 0.05}, "inp", (2, 2))
     stream = native.default_stream()
     for _ in range(warmup):
         step()
@@ -519,7 +526,7 @@ def run_b200(args, dist):
     from paper_2311_08322_b200 import native, workloads
 
     if dist.world > 1:
-        native.set_device(dist.local)
+        native.set_device(dist.local % native.device_count() if dist.shared else dist.local)
     dev = native.require_device()
     kernel, dtype, domain = WORKLOADS[args.workload]
     st = b200.compile_stencil(workloads.source(kernel, dtype), kernel)
@@ -564,7 +571,9 @@ def run_b200(args, dist):
         "clocks": sampler.summary(),
     }
     decomp_line = None
-    if not args.no_extra:
+    if dist.shared and dist.world > 1:
+        decomp_line = {"skipped": "GTS_BENCH_SHARED_GPU: NCCL cannot run two ranks on one GPU"}
+    elif not args.no_extra:
         try:
             ms_d, gdom, grid, lps = decomposed_hdiff(dist, max(args.steps // 4, 20), args.warmup)
             pts_d = gdom[0] * gdom[1] * gdom[2]
@@ -579,8 +588,24 @@ def run_b200(args, dist):
             }
         except Exception as exc:  # pragma: no cover - reported, not fatal
             decomp_line = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+    peer_line = None
+    if not args.no_extra and dist.world > 1:
+        try:
+            ms_p, gdom, grid, lps = decomposed_hdiff(dist, max(args.steps // 4, 20), args.warmup,
+                                                     transport="peer")
+            alg_p = workloads.algorithmic_bytes("hdiff", (512, 1024, 80), "f64")
+            peer_line = {
+                "workload": "horizontal diffusion float64, 512x1024x80 per GPU, decomposed "
+                            f"{grid[0]}x{grid[1]} (global {gdom[0]}x{gdom[1]}x{gdom[2]}), halo exchange by "
+                            "CUDA-IPC peer stores + step flags (no NCCL), overlapped with the interior",
+                "value": gdom[0] * gdom[1] * gdom[2] / (ms_p / 1e3), "unit": "grid-points/s",
+                "ms_per_step": ms_p, "achieved_gbs_per_gpu": alg_p / (ms_p / 1e3) / 1e9,
+                "launches_per_step": lps, "scaling": "weak",
+            }
+        except Exception as exc:  # pragma: no cover - reported, not fatal
+            peer_line = {"error": f"{type(exc).__name__}: {exc}"[:300]}
     if dist.rank == 0 and dist.world > 1:
-        line["extra"] = {"hdiff_decomposed": decomp_line}
+        line["extra"] = {"hdiff_decomposed": decomp_line, "hdiff_decomposed_peer": peer_line}
     if dist.rank == 0 and dist.world == 1 and not args.no_extra:
         extra = {}
         for name in ("hdiff", "hdiff32"):

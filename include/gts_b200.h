@@ -123,6 +123,28 @@ int gts_b200_graph_end(void* stream, void** exec);
 int gts_b200_graph_launch(void* exec, void* stream);
 int gts_b200_graph_destroy(void* exec);
 
+/* Peer-memory halo exchange between the processes of one node (no NCCL on
+ * the data path; decomp.PeerHaloExchanger).  Replaces the reference's absent
+ * multi-process path (stencilforge SPEC.md:12) the way gen's entry
+ * (gen.py:5-14) is replaced above: plain pointers, element strides, a stream.
+ *  - ipc_get_handle / ipc_open / ipc_close: share a device allocation (64-B
+ *    opaque handle) with another process; opened with lazy peer access, so
+ *    the pointer is P2P over NVLink / NVSwitch when the owner is another GPU;
+ *  - copy_box: strided 3-D box -> strided 3-D box (dst / src point at the
+ *    boxes' first elements; either side may be a peer pointer);
+ *  - flag_signal: after everything earlier on ``stream``, store ``value`` to
+ *    a (possibly peer) 64-bit flag with system-scope release;
+ *  - flag_wait: ``stream`` waits until the flag is >= ``value``
+ *    (system-scope acquire spin). */
+int gts_b200_ipc_get_handle(const void* dptr, void* handle64);
+int gts_b200_ipc_open(const void* handle64, void** dptr);
+int gts_b200_ipc_close(void* dptr);
+int gts_b200_copy_box(void* dst, int64_t d_i, int64_t d_j, int64_t d_k, const void* src,
+                      int64_t s_i, int64_t s_j, int64_t s_k, int64_t ni, int64_t nj, int64_t nk,
+                      int itemsize, void* stream);
+int gts_b200_flag_signal(void* flag, uint64_t value, void* stream);
+int gts_b200_flag_wait(const void* flag, uint64_t value, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <string.h>
 
 #include <mutex>
 
@@ -241,4 +242,92 @@ GTS_EXPORT int gts_b200_memcpy2d_d2h(void* dst, size_t dpitch, const void* src, 
 }
 GTS_EXPORT int gts_b200_stream_wait_event(void* stream, void* event) {
   return (int)cudaStreamWaitEvent((cudaStream_t)stream, (cudaEvent_t)event, 0);
+}
+
+// ---------------------------------------------------------------------------
+// Peer-memory halo exchange (decomp.PeerHaloExchanger): fields and flag words
+// are shared between the processes of one node with CUDA IPC; a rank writes
+// its boundary rows straight into the neighbour's halo (P2P stores over
+// NVLink / NVSwitch between GPUs, plain stores when both ranks share a
+// device), then raises a flag in the neighbour's memory with a system-scope
+// release; the consumer's stream waits on the flag with an acquire spin.
+// Flags carry the step number, so no host synchronisation is needed per step.
+// ---------------------------------------------------------------------------
+GTS_EXPORT int gts_b200_ipc_get_handle(const void* dptr, void* handle64) {
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, (void*)dptr);
+  if (e != cudaSuccess) return (int)e;
+  memcpy(handle64, &h, sizeof(h) < 64 ? sizeof(h) : 64);
+  return 0;
+}
+
+GTS_EXPORT int gts_b200_ipc_open(const void* handle64, void** dptr) {
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, sizeof(h) < 64 ? sizeof(h) : 64);
+  return (int)cudaIpcOpenMemHandle(dptr, h, cudaIpcMemLazyEnablePeerAccess);
+}
+
+GTS_EXPORT int gts_b200_ipc_close(void* dptr) { return (int)cudaIpcCloseMemHandle(dptr); }
+
+template <typename T>
+__global__ void gts_copy_box_kernel(T* dst, int64_t d_i, int64_t d_j, int64_t d_k, const T* src,
+                                    int64_t s_i, int64_t s_j, int64_t s_k, int64_t ni, int64_t nj,
+                                    int64_t nk) {
+  const int64_t n = ni * nj * nk;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = t % nj;
+    const int64_t r = t / nj;
+    const int64_t i = r % ni;
+    const int64_t k = r / ni;
+    dst[i * d_i + j * d_j + k * d_k] = src[i * s_i + j * s_j + k * s_k];
+  }
+}
+
+// dst / src point at the boxes' first elements; strides in elements.
+GTS_EXPORT int gts_b200_copy_box(void* dst, int64_t d_i, int64_t d_j, int64_t d_k, const void* src,
+                                 int64_t s_i, int64_t s_j, int64_t s_k, int64_t ni, int64_t nj,
+                                 int64_t nk, int itemsize, void* stream) {
+  const int64_t n = ni * nj * nk;
+  if (n <= 0) return 0;
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (itemsize == 8)
+    gts_copy_box_kernel<unsigned long long><<<(unsigned)blocks, 256, 0, st>>>(
+        (unsigned long long*)dst, d_i, d_j, d_k, (const unsigned long long*)src, s_i, s_j, s_k,
+        ni, nj, nk);
+  else if (itemsize == 4)
+    gts_copy_box_kernel<unsigned int><<<(unsigned)blocks, 256, 0, st>>>(
+        (unsigned int*)dst, d_i, d_j, d_k, (const unsigned int*)src, s_i, s_j, s_k, ni, nj, nk);
+  else
+    return (int)cudaErrorInvalidValue;
+  return (int)cudaGetLastError();
+}
+
+__global__ void gts_flag_signal_kernel(unsigned long long* flag, unsigned long long value) {
+  // every prior kernel on this stream has completed (stream order); the
+  // system-scope release makes its stores visible before the flag
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flag), "l"(value) : "memory");
+}
+
+__global__ void gts_flag_wait_kernel(const unsigned long long* flag, unsigned long long value) {
+  unsigned long long v;
+  for (;;) {
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flag) : "memory");
+    if (v >= value) break;
+    __nanosleep(256);
+  }
+}
+
+GTS_EXPORT int gts_b200_flag_signal(void* flag, uint64_t value, void* stream) {
+  gts_flag_signal_kernel<<<1, 1, 0, (cudaStream_t)stream>>>((unsigned long long*)flag,
+                                                            (unsigned long long)value);
+  return (int)cudaGetLastError();
+}
+
+GTS_EXPORT int gts_b200_flag_wait(const void* flag, uint64_t value, void* stream) {
+  gts_flag_wait_kernel<<<1, 1, 0, (cudaStream_t)stream>>>((const unsigned long long*)flag,
+                                                          (unsigned long long)value);
+  return (int)cudaGetLastError();
 }

@@ -306,3 +306,191 @@ class DecomposedStep:
             self.compute.wait_stream(self.comm)
         for go in self.boundary:
             go()
+
+
+# ---------------------------------------------------------------------------
+# Peer-memory transport (no NCCL on the data path)
+# ---------------------------------------------------------------------------
+# direction index d of a face neighbour, and the direction it sees us in
+DIRS = ((-1, 0), (1, 0), (0, -1), (0, 1))  # i-lo, i-hi, j-lo, j-hi
+OPP = (1, 0, 3, 2)
+ARRIVED, ACKED = 0, 4  # flag word = base + d: "halo from d landed (step)", "d consumed my puts (step)"
+
+
+def face_puts(decomp: Decomposition, halo: tuple, axis: str) -> list:
+    """The face copies of one exchange phase, as (direction, src box in my
+    storage, dst box origin in the neighbour's storage, box size): my
+    boundary rows go straight into the neighbour's halo.  Phase "i" covers the
+    interior columns plus the global j-halo columns; phase "j" the full
+    storage height including the i-halo rows received in phase "i", so
+    corners arrive without diagonal messages.  Unlike HaloExchanger (where
+    the receiver unpacks in order) two ranks write into one halo here, so the
+    boxes never overlap."""
+    ni, nj, nk = decomp.local_domain
+    hi, hj = halo
+    out = []
+    for d in ((0, 1) if axis == "i" else (2, 3)):
+        nb = decomp.neighbour(*DIRS[d])
+        if nb is None:
+            continue
+        nd = Decomposition(decomp.global_domain, decomp.grid, nb)
+        nni, nnj, _ = nd.local_domain
+        if axis == "i":
+            if hi == 0:
+                continue
+            # j-halo columns that a j-neighbour rewrites in phase j are left
+            # out: the two writes come from different ranks, unordered, and
+            # phase j carries the right (diagonal) values; the global j-halo
+            # columns travel here (an i-neighbour shares our j-neighbours)
+            c0 = hj if decomp.neighbour(0, -1) is not None else 0
+            c1 = nj + hj if decomp.neighbour(0, 1) is not None else nj + 2 * hj
+            size = (hi, c1 - c0, nk)
+            src = (hi, c0, 0) if d == 0 else (ni, c0, 0)
+            dst = (nni + hi, c0, 0) if d == 0 else (0, c0, 0)
+        else:
+            if hj == 0:
+                continue
+            size = (ni + 2 * hi, hj, nk)
+            src = (0, hj, 0) if d == 2 else (0, nj, 0)
+            dst = (0, nnj + hj, 0) if d == 2 else (0, 0, 0)
+        out.append((d, nb, src, dst, size))
+    return out
+
+
+class PeerHaloExchanger:
+    """Halo refresh of one device field by direct peer-memory puts.
+
+    Every rank shares its field allocation and a 64-byte flag block with its
+    face neighbours through CUDA IPC (handles exchanged once over
+    ``torch.distributed``).  Per step ``s`` on the exchange stream:
+
+    * phase i: for each i-neighbour, wait until it acknowledged step s-1
+      (its boundary strips no longer read the halo we are about to rewrite),
+      copy our boundary rows straight into its halo (P2P stores over NVLink /
+      NVSwitch, ``gts_b200_copy_box``), then raise its ARRIVED flag to s
+      (system-scope release, ``gts_b200_flag_signal``); wait for our own
+      i-halos (ARRIVED >= s);
+    * phase j: the same for the j-neighbours over the full height (corners
+      travel with the i-halo rows received in phase i); wait for our j-halos.
+
+    ``acknowledge`` (after the boundary strips, on the compute stream) raises
+    each neighbour's ACKED flag.  Flags carry the step number, so steps need
+    no host synchronisation and no NCCL call; the only collective is the
+    one-off handle exchange."""
+
+    def __init__(self, decomp: Decomposition, halo: tuple, field, stream: int, group=None):
+        import ctypes
+
+        import torch.distributed as dist
+
+        from . import native, storage
+
+        if not hasattr(field, "_buf"):
+            raise TypeError("PeerHaloExchanger needs a DeviceFieldStorage that owns its allocation")
+        self.native, self.decomp, self.halo, self.field = native, decomp, tuple(halo), field
+        self.stream = stream
+        self.step = 0
+        self._flags = storage._DeviceBuffer(64, pinned_host=False)
+        native.call("gts_b200_memset", self._flags.dptr, 0, 64, stream)
+        native.synchronize(stream)
+
+        def handle(ptr):
+            h = ctypes.create_string_buffer(64)
+            native.call("gts_b200_ipc_get_handle", ptr, h)
+            return h.raw
+
+        me = {"field": handle(field._buf.dptr), "offset": field.base_address() - field._buf.dptr,
+              "strides": tuple(field.strides), "flags": handle(self._flags.dptr)}
+        world = dist.get_world_size(group)
+        allv = [None] * world
+        dist.all_gather_object(allv, me, group=group)
+        self._opened = []
+        self.peer = {}
+        for d in range(4):
+            nb = decomp.neighbour(*DIRS[d])
+            if nb is None:
+                continue
+            info = allv[nb]
+            fp, gp = ctypes.c_void_p(), ctypes.c_void_p()
+            native.call("gts_b200_ipc_open", info["field"], ctypes.byref(fp))
+            native.call("gts_b200_ipc_open", info["flags"], ctypes.byref(gp))
+            self._opened += [fp.value, gp.value]
+            self.peer[d] = (fp.value + info["offset"], info["strides"], gp.value)
+        self.puts = {ax: face_puts(decomp, self.halo, ax) for ax in ("i", "j")}
+        dist.barrier(group)  # every rank mapped its peers before anyone signals
+
+    def _flag(self, base: int, word: int) -> int:
+        return base + 8 * word
+
+    def exchange_async(self) -> None:
+        """Enqueue one halo refresh on the exchange stream (no host sync)."""
+        self.step += 1
+        s, st, f = self.step, self.stream, self.field
+        item = f.itemsize
+        for axis in ("i", "j"):
+            for d, nb, src, dst, size in self.puts[axis]:
+                base, strides, pflags = self.peer[d]
+                self.native.call("gts_b200_flag_wait", self._flag(self._flags.dptr, ACKED + d), s - 1, st)
+                so = sum(a * b for a, b in zip(src, f.strides))
+                do = sum(a * b for a, b in zip(dst, strides))
+                self.native.call("gts_b200_copy_box", base + do * item, *strides,
+                                 f.base_address() + so * item, *f.strides, *size, item, st)
+                self.native.call("gts_b200_flag_signal", self._flag(pflags, ARRIVED + OPP[d]), s, st)
+            for d, *_ in self.puts[axis]:
+                self.native.call("gts_b200_flag_wait", self._flag(self._flags.dptr, ARRIVED + d), s, st)
+
+    def acknowledge(self, stream: int) -> None:
+        """After the step's halo readers on ``stream``: neighbours may rewrite
+        our halos for the next step."""
+        for d, (base, strides, pflags) in self.peer.items():
+            self.native.call("gts_b200_flag_signal", self._flag(pflags, ACKED + OPP[d]), self.step, stream)
+
+    def close(self) -> None:
+        for p in self._opened:
+            try:
+                self.native.call("gts_b200_ipc_close", p)
+            except Exception:  # pragma: no cover - teardown
+                pass
+        self._opened = []
+
+
+class PeerDecomposedStep:
+    """DecomposedStep over the peer-memory transport: the halo exchange
+    (PeerHaloExchanger, its own stream) overlaps the interior on the compute
+    stream; the boundary strips wait for it through an event; the step ends
+    by acknowledging the neighbours.  Native streams and events only."""
+
+    def __init__(self, stencil, decomposition: Decomposition, fields: dict, scalars: dict,
+                 halo_field: str, halo: tuple, group=None):
+        from . import native
+
+        self.native = native
+        self.compute = native.default_stream()
+        self.comm = native.aux_stream("peer-halo")
+        module = stencil.build_info["module"]
+        dom = decomposition.local_domain
+        self.exchanger = PeerHaloExchanger(decomposition, halo, fields[halo_field], self.comm, group)
+        parts = strips(dom, halo) if self.exchanger.peer else [("all", (0, 0), dom)]
+        cs = self.compute
+        self.interior = [module.launcher(size, fields, scalars, cs, (off[0], off[1], 0))
+                         for name, off, size in parts if name in ("interior", "all")]
+        self.boundary = [module.launcher(size, fields, scalars, cs, (off[0], off[1], 0))
+                         for name, off, size in parts if name not in ("interior", "all")]
+        self.launches_per_step = len(self.interior) + len(self.boundary)
+        self._ev_start, self._ev_halo = native.Event(), native.Event()
+
+    def __call__(self) -> None:
+        n = self.native
+        if self.exchanger.peer:
+            self._ev_start.record(self.compute)  # the field is final for this step
+            n.call("gts_b200_stream_wait_event", self.comm, self._ev_start.ptr)
+            self.exchanger.exchange_async()
+            self._ev_halo.record(self.comm)
+        for go in self.interior:
+            go()
+        if self.exchanger.peer:
+            n.call("gts_b200_stream_wait_event", self.compute, self._ev_halo.ptr)
+        for go in self.boundary:
+            go()
+        if self.exchanger.peer:
+            self.exchanger.acknowledge(self.compute)

@@ -58,6 +58,12 @@ SIGNATURES = {
     "gts_b200_graph_end": (_INT, [_VP, _c.POINTER(_VP)]),
     "gts_b200_graph_launch": (_INT, [_VP, _VP]),
     "gts_b200_graph_destroy": (_INT, [_VP]),
+    "gts_b200_ipc_get_handle": (_INT, [_VP, _VP]),
+    "gts_b200_ipc_open": (_INT, [_VP, _c.POINTER(_VP)]),
+    "gts_b200_ipc_close": (_INT, [_VP]),
+    "gts_b200_copy_box": (_INT, [_VP] + [_I64] * 3 + [_VP] + [_I64] * 6 + [_INT, _VP]),
+    "gts_b200_flag_signal": (_INT, [_VP, _c.c_uint64, _VP]),
+    "gts_b200_flag_wait": (_INT, [_VP, _c.c_uint64, _VP]),
 }
 
 _lib: Optional[ctypes.CDLL] = None
