@@ -88,6 +88,9 @@ int gts_b200_stream_synchronize(void* stream);
 int gts_b200_event_create(void** event);
 int gts_b200_event_destroy(void* event);
 int gts_b200_event_record(void* event, void* stream);
+/* Plain record for cross-stream ordering: inside a stream capture it is an
+ * intra-graph dependency (fork / join), not an event-record node. */
+int gts_b200_event_record_dep(void* event, void* stream);
 int gts_b200_event_synchronize(void* event);
 int gts_b200_event_elapsed_ms(float* ms, void* start, void* end);
 
@@ -128,21 +131,28 @@ int gts_b200_graph_destroy(void* exec);
  * multi-process path (stencilforge SPEC.md:12) the way gen's entry
  * (gen.py:5-14) is replaced above: plain pointers, element strides, a stream.
  *  - ipc_get_handle / ipc_open / ipc_close: share a device allocation (64-B
- *    opaque handle) with another process; opened with lazy peer access, so
- *    the pointer is P2P over NVLink / NVSwitch when the owner is another GPU;
+ *    opaque handle + the byte offset of ``dptr`` from the allocation base,
+ *    which ipc_open returns) with another process; opened with lazy peer
+ *    access, so the pointer is P2P over NVLink / NVSwitch when the owner is
+ *    another GPU;
  *  - copy_box: strided 3-D box -> strided 3-D box (dst / src point at the
  *    boxes' first elements; either side may be a peer pointer);
  *  - flag_signal: after everything earlier on ``stream``, store ``value`` to
  *    a (possibly peer) 64-bit flag with system-scope release;
  *  - flag_wait: ``stream`` waits until the flag is >= ``value``
  *    (system-scope acquire spin). */
-int gts_b200_ipc_get_handle(const void* dptr, void* handle64);
+int gts_b200_ipc_get_handle(const void* dptr, void* handle64, size_t* offset);
 int gts_b200_ipc_open(const void* handle64, void** dptr);
 int gts_b200_ipc_close(void* dptr);
 int gts_b200_copy_box(void* dst, int64_t d_i, int64_t d_j, int64_t d_k, const void* src,
                       int64_t s_i, int64_t s_j, int64_t s_k, int64_t ni, int64_t nj, int64_t nk,
                       int itemsize, void* stream);
 int gts_b200_flag_signal(void* flag, uint64_t value, void* stream);
+/* Graph-capturable forms: flag_add adds 1 (system-scope release);
+ * flag_wait_next bumps the consumer's own expected count (a 64-bit word in
+ * device memory) and waits until the flag reaches it. */
+int gts_b200_flag_add(void* flag, void* stream);
+int gts_b200_flag_wait_next(const void* flag, void* expected, void* stream);
 int gts_b200_flag_wait(const void* flag, uint64_t value, void* stream);
 
 #ifdef __cplusplus

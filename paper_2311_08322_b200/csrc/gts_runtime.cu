@@ -93,6 +93,12 @@ GTS_EXPORT int gts_b200_event_record(void* event, void* stream) {
                                          cudaEventRecordExternal);
   return (int)cudaEventRecord((cudaEvent_t)event, (cudaStream_t)stream);
 }
+// Cross-stream ordering marker: a plain record, which inside a stream capture
+// becomes an intra-graph dependency (fork / join of a captured multi-stream
+// step), not an event-record node.
+GTS_EXPORT int gts_b200_event_record_dep(void* event, void* stream) {
+  return (int)cudaEventRecord((cudaEvent_t)event, (cudaStream_t)stream);
+}
 GTS_EXPORT int gts_b200_event_synchronize(void* event) {
   return (int)cudaEventSynchronize((cudaEvent_t)event);
 }
@@ -253,9 +259,28 @@ GTS_EXPORT int gts_b200_stream_wait_event(void* stream, void* event) {
 // release; the consumer's stream waits on the flag with an acquire spin.
 // Flags carry the step number, so no host synchronisation is needed per step.
 // ---------------------------------------------------------------------------
-GTS_EXPORT int gts_b200_ipc_get_handle(const void* dptr, void* handle64) {
+// The handle names the whole underlying allocation, and ipc_open returns its
+// base: cudaMalloc may place a small allocation inside a larger block, so
+// the byte offset of ``dptr`` from that base is returned as well (driver
+// cuMemGetAddressRange through the runtime's entry-point query).
+typedef int (*gts_mem_range_fn)(unsigned long long*, size_t*, unsigned long long);
+
+GTS_EXPORT int gts_b200_ipc_get_handle(const void* dptr, void* handle64, size_t* offset) {
+  static gts_mem_range_fn range = nullptr;
+  if (!range) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return (int)cudaErrorNotSupported;
+    range = (gts_mem_range_fn)p;
+  }
+  unsigned long long base = 0;
+  size_t size = 0;
+  if (range(&base, &size, (unsigned long long)(uintptr_t)dptr) != 0) return (int)cudaErrorInvalidValue;
+  *offset = (size_t)((uintptr_t)dptr - (uintptr_t)base);
   cudaIpcMemHandle_t h;
-  cudaError_t e = cudaIpcGetMemHandle(&h, (void*)dptr);
+  cudaError_t e = cudaIpcGetMemHandle(&h, (void*)(uintptr_t)base);
   if (e != cudaSuccess) return (int)e;
   memcpy(handle64, &h, sizeof(h) < 64 ? sizeof(h) : 64);
   return 0;
@@ -318,6 +343,36 @@ __global__ void gts_flag_wait_kernel(const unsigned long long* flag, unsigned lo
     if (v >= value) break;
     __nanosleep(256);
   }
+}
+
+// Step-agnostic forms (CUDA-graph capturable: no per-step arguments): the
+// producer adds 1 to the flag; the consumer keeps its own expected count in
+// device memory, bumps it and waits until the flag reaches it.
+__global__ void gts_flag_add_kernel(unsigned long long* flag) {
+  asm volatile("red.release.sys.global.add.u64 [%0], 1;" ::"l"(flag) : "memory");
+}
+
+__global__ void gts_flag_wait_next_kernel(const unsigned long long* flag,
+                                          unsigned long long* expected) {
+  const unsigned long long e = *expected + 1ull;
+  *expected = e;
+  unsigned long long v;
+  for (;;) {
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flag) : "memory");
+    if ((long long)(v - e) >= 0) break;
+    __nanosleep(256);
+  }
+}
+
+GTS_EXPORT int gts_b200_flag_add(void* flag, void* stream) {
+  gts_flag_add_kernel<<<1, 1, 0, (cudaStream_t)stream>>>((unsigned long long*)flag);
+  return (int)cudaGetLastError();
+}
+
+GTS_EXPORT int gts_b200_flag_wait_next(const void* flag, void* expected, void* stream) {
+  gts_flag_wait_next_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(
+      (const unsigned long long*)flag, (unsigned long long*)expected);
+  return (int)cudaGetLastError();
 }
 
 GTS_EXPORT int gts_b200_flag_signal(void* flag, uint64_t value, void* stream) {

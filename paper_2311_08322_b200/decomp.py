@@ -362,21 +362,26 @@ class PeerHaloExchanger:
 
     Every rank shares its field allocation and a 64-byte flag block with its
     face neighbours through CUDA IPC (handles exchanged once over
-    ``torch.distributed``).  Per step ``s`` on the exchange stream:
+    ``torch.distributed``).  The flags are counters: ARRIVED[d] counts the
+    halo puts received from the neighbour in direction d, ACKED[d] the steps
+    that neighbour has finished reading what we put.  Per step, on the
+    exchange stream:
 
-    * phase i: for each i-neighbour, wait until it acknowledged step s-1
-      (its boundary strips no longer read the halo we are about to rewrite),
-      copy our boundary rows straight into its halo (P2P stores over NVLink /
-      NVSwitch, ``gts_b200_copy_box``), then raise its ARRIVED flag to s
-      (system-scope release, ``gts_b200_flag_signal``); wait for our own
-      i-halos (ARRIVED >= s);
+    * phase i: for each i-neighbour, wait until it acknowledged the previous
+      step (its boundary strips no longer read the halo we are about to
+      rewrite), copy our boundary rows straight into its halo (P2P stores over
+      NVLink / NVSwitch, ``gts_b200_copy_box``), then add 1 to its ARRIVED
+      flag (system-scope release, ``gts_b200_flag_add``); wait for our own
+      i-halos;
     * phase j: the same for the j-neighbours over the full height (corners
       travel with the i-halo rows received in phase i); wait for our j-halos.
 
-    ``acknowledge`` (after the boundary strips, on the compute stream) raises
-    each neighbour's ACKED flag.  Flags carry the step number, so steps need
-    no host synchronisation and no NCCL call; the only collective is the
-    one-off handle exchange."""
+    ``acknowledge`` (after the boundary strips, on the compute stream) bumps
+    each neighbour's ACKED flag.  Each wait bumps a private expected count
+    in device memory (``gts_b200_flag_wait_next``), so no launch carries a
+    step number: a step needs no host synchronisation, no NCCL call, and can
+    be captured once into a CUDA graph and replayed.  The only collective is
+    the one-off handle exchange."""
 
     def __init__(self, decomp: Decomposition, halo: tuple, field, stream: int, group=None):
         import ctypes
@@ -385,22 +390,25 @@ class PeerHaloExchanger:
 
         from . import native, storage
 
-        if not hasattr(field, "_buf"):
-            raise TypeError("PeerHaloExchanger needs a DeviceFieldStorage that owns its allocation")
+        if not isinstance(field, storage.DeviceFieldStorage):
+            raise TypeError("PeerHaloExchanger needs a DeviceFieldStorage")
         self.native, self.decomp, self.halo, self.field = native, decomp, tuple(halo), field
         self.stream = stream
-        self.step = 0
-        self._flags = storage._DeviceBuffer(64, pinned_host=False)
+        self._flags = storage._DeviceBuffer(64, pinned_host=False)  # shared: ARRIVED[4], ACKED[4]
+        self._expect = storage._DeviceBuffer(64, pinned_host=False)  # private expected counts
         native.call("gts_b200_memset", self._flags.dptr, 0, 64, stream)
+        native.call("gts_b200_memset", self._expect.dptr, 0, 32, stream)
+        # the first ACKED wait must pass at once: expected = -1 (+1 -> 0)
+        native.call("gts_b200_memset", self._expect.dptr + 32, 0xFF, 32, stream)
         native.synchronize(stream)
 
         def handle(ptr):
-            h = ctypes.create_string_buffer(64)
-            native.call("gts_b200_ipc_get_handle", ptr, h)
-            return h.raw
+            h, off = ctypes.create_string_buffer(64), ctypes.c_size_t()
+            native.call("gts_b200_ipc_get_handle", ptr, h, ctypes.byref(off))
+            return h.raw, off.value
 
-        me = {"field": handle(field._buf.dptr), "offset": field.base_address() - field._buf.dptr,
-              "strides": tuple(field.strides), "flags": handle(self._flags.dptr)}
+        me = {"field": handle(field.base_address()), "strides": tuple(field.strides),
+              "flags": handle(self._flags.dptr)}
         world = dist.get_world_size(group)
         allv = [None] * world
         dist.all_gather_object(allv, me, group=group)
@@ -412,38 +420,42 @@ class PeerHaloExchanger:
                 continue
             info = allv[nb]
             fp, gp = ctypes.c_void_p(), ctypes.c_void_p()
-            native.call("gts_b200_ipc_open", info["field"], ctypes.byref(fp))
-            native.call("gts_b200_ipc_open", info["flags"], ctypes.byref(gp))
+            native.call("gts_b200_ipc_open", info["field"][0], ctypes.byref(fp))
+            native.call("gts_b200_ipc_open", info["flags"][0], ctypes.byref(gp))
             self._opened += [fp.value, gp.value]
-            self.peer[d] = (fp.value + info["offset"], info["strides"], gp.value)
+            self.peer[d] = (fp.value + info["field"][1], info["strides"], gp.value + info["flags"][1])
         self.puts = {ax: face_puts(decomp, self.halo, ax) for ax in ("i", "j")}
         dist.barrier(group)  # every rank mapped its peers before anyone signals
 
-    def _flag(self, base: int, word: int) -> int:
+    @staticmethod
+    def _word(base: int, word: int) -> int:
         return base + 8 * word
+
+    def _wait(self, word: int, stream: int) -> None:
+        self.native.call("gts_b200_flag_wait_next", self._word(self._flags.dptr, word),
+                         self._word(self._expect.dptr, word), stream)
 
     def exchange_async(self) -> None:
         """Enqueue one halo refresh on the exchange stream (no host sync)."""
-        self.step += 1
-        s, st, f = self.step, self.stream, self.field
+        st, f = self.stream, self.field
         item = f.itemsize
         for axis in ("i", "j"):
             for d, nb, src, dst, size in self.puts[axis]:
                 base, strides, pflags = self.peer[d]
-                self.native.call("gts_b200_flag_wait", self._flag(self._flags.dptr, ACKED + d), s - 1, st)
+                self._wait(ACKED + d, st)
                 so = sum(a * b for a, b in zip(src, f.strides))
                 do = sum(a * b for a, b in zip(dst, strides))
                 self.native.call("gts_b200_copy_box", base + do * item, *strides,
                                  f.base_address() + so * item, *f.strides, *size, item, st)
-                self.native.call("gts_b200_flag_signal", self._flag(pflags, ARRIVED + OPP[d]), s, st)
+                self.native.call("gts_b200_flag_add", self._word(pflags, ARRIVED + OPP[d]), st)
             for d, *_ in self.puts[axis]:
-                self.native.call("gts_b200_flag_wait", self._flag(self._flags.dptr, ARRIVED + d), s, st)
+                self._wait(ARRIVED + d, st)
 
     def acknowledge(self, stream: int) -> None:
         """After the step's halo readers on ``stream``: neighbours may rewrite
         our halos for the next step."""
         for d, (base, strides, pflags) in self.peer.items():
-            self.native.call("gts_b200_flag_signal", self._flag(pflags, ACKED + OPP[d]), self.step, stream)
+            self.native.call("gts_b200_flag_add", self._word(pflags, ACKED + OPP[d]), stream)
 
     def close(self) -> None:
         for p in self._opened:
@@ -470,6 +482,8 @@ class PeerDecomposedStep:
         module = stencil.build_info["module"]
         dom = decomposition.local_domain
         self.exchanger = PeerHaloExchanger(decomposition, halo, fields[halo_field], self.comm, group)
+        self.fields = fields
+        self.written = sorted(module.written)
         parts = strips(dom, halo) if self.exchanger.peer else [("all", (0, 0), dom)]
         cs = self.compute
         self.interior = [module.launcher(size, fields, scalars, cs, (off[0], off[1], 0))
@@ -479,13 +493,35 @@ class PeerDecomposedStep:
         self.launches_per_step = len(self.interior) + len(self.boundary)
         self._ev_start, self._ev_halo = native.Event(), native.Event()
 
+    def graph(self, steps: int):
+        """``steps`` steps captured once into a CUDA graph on the compute
+        stream (the exchange stream joins the capture through the fork / join
+        events); replay with ``.launch()``."""
+        g = self.native.Graph(self.compute)
+        with g.capture():
+            for _ in range(steps):
+                self()
+        written = [self.fields[n] for n in self.written]
+        peer = self.exchanger.field
+
+        class _Replay:
+            graph = g
+
+            def launch(self_) -> None:
+                g.launch()
+                for w in written:  # storages written by the replay: host mirrors are stale
+                    w.mark_device_written()
+                peer.mark_device_written()  # neighbours rewrote its halo
+
+        return _Replay()
+
     def __call__(self) -> None:
         n = self.native
         if self.exchanger.peer:
-            self._ev_start.record(self.compute)  # the field is final for this step
+            self._ev_start.record_dep(self.compute)  # the field is final for this step
             n.call("gts_b200_stream_wait_event", self.comm, self._ev_start.ptr)
             self.exchanger.exchange_async()
-            self._ev_halo.record(self.comm)
+            self._ev_halo.record_dep(self.comm)
         for go in self.interior:
             go()
         if self.exchanger.peer:
@@ -494,3 +530,4 @@ class PeerDecomposedStep:
             go()
         if self.exchanger.peer:
             self.exchanger.acknowledge(self.compute)
+            self.exchanger.field.mark_device_written()  # neighbours rewrote its halo

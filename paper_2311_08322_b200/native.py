@@ -47,6 +47,7 @@ SIGNATURES = {
     "gts_b200_event_destroy": (_INT, [_VP]),
     "gts_b200_event_record": (_INT, [_VP, _VP]),
     "gts_b200_event_synchronize": (_INT, [_VP]),
+    "gts_b200_event_record_dep": (_INT, [_VP, _VP]),
     "gts_b200_event_elapsed_ms": (_INT, [_c.POINTER(_c.c_float), _VP, _VP]),
     "gts_b200_l2_flush": (_INT, [_VP]),
     "gts_b200_pack_box": (_INT, [_VP, _VP] + [_I64] * 9 + [_INT, _VP]),
@@ -58,12 +59,14 @@ SIGNATURES = {
     "gts_b200_graph_end": (_INT, [_VP, _c.POINTER(_VP)]),
     "gts_b200_graph_launch": (_INT, [_VP, _VP]),
     "gts_b200_graph_destroy": (_INT, [_VP]),
-    "gts_b200_ipc_get_handle": (_INT, [_VP, _VP]),
+    "gts_b200_ipc_get_handle": (_INT, [_VP, _VP, _c.POINTER(_SZ)]),
     "gts_b200_ipc_open": (_INT, [_VP, _c.POINTER(_VP)]),
     "gts_b200_ipc_close": (_INT, [_VP]),
     "gts_b200_copy_box": (_INT, [_VP] + [_I64] * 3 + [_VP] + [_I64] * 6 + [_INT, _VP]),
     "gts_b200_flag_signal": (_INT, [_VP, _c.c_uint64, _VP]),
     "gts_b200_flag_wait": (_INT, [_VP, _c.c_uint64, _VP]),
+    "gts_b200_flag_add": (_INT, [_VP, _VP]),
+    "gts_b200_flag_wait_next": (_INT, [_VP, _VP, _VP]),
 }
 
 _lib: Optional[ctypes.CDLL] = None
@@ -217,6 +220,10 @@ class Event:
 
     def record(self, stream: Optional[int] = None) -> None:
         call("gts_b200_event_record", self.ptr, stream if stream is not None else default_stream())
+
+    def record_dep(self, stream: int) -> None:
+        """Cross-stream ordering marker (captures as a graph dependency)."""
+        call("gts_b200_event_record_dep", self.ptr, stream)
 
     def synchronize(self) -> None:
         call("gts_b200_event_synchronize", self.ptr)

@@ -59,10 +59,51 @@ def main():
     for _ in range(steps):
         step()
     native.synchronize(step.compute)
+    if os.environ.get("PEER_DEBUG"):
+        import ctypes
+        full = d.scatter(g, (2, 2))
+        have = inp.host_array()
+        ow = out.host_array()
+        wv = oracle.hdiff_c(g, 0.05)[d.i0: d.i1, d.j0: d.j1]
+        ob = np.argwhere(ow != wv)
+        print(f"DEBUG rank {rank} out bad {len(ob)} rows {sorted(set(ob[:, 0].tolist()))[:10]}", flush=True)
+        bad = ~((have == full) | (np.isnan(have) & np.isnan(full)))
+        fl = (ctypes.c_uint64 * 8)()
+        native.call("gts_b200_memcpy_d2h", ctypes.addressof(fl), step.exchanger._flags.dptr, 64, step.compute)
+        ex = (ctypes.c_uint64 * 8)()
+        native.call("gts_b200_memcpy_d2h", ctypes.addressof(ex), step.exchanger._expect.dptr, 64, step.compute)
+        native.synchronize(step.compute)
+        idx = np.argwhere(bad)
+        print(f"DEBUG rank {rank} bad {int(bad.sum())} nan {int(np.isnan(have).sum())} "
+              f"rows {sorted(set(idx[:, 0].tolist()))[:8]} cols {sorted(set(idx[:, 1].tolist()))[:8]} "
+              f"flags {list(fl)} expect {list(ex)} peers { {k: (hex(v[0]), v[1], hex(v[2])) for k, v in step.exchanger.peer.items()} }",
+              flush=True)
     want = oracle.hdiff_c(g, 0.05)[d.i0: d.i1, d.j0: d.j1]
     got = out.host_array()
     ok = bool(np.array_equal(got, want))
-    line = f"rank {rank} grid {grid} local {d.local_domain} steps {steps} bitwise {ok}"
+    # the same steps captured in a CUDA graph, replayed twice, after the
+    # neighbour-owned halo cells were poisoned again and the output zeroed
+    gr = step.graph(steps)
+    native.synchronize(step.compute)
+    dist.barrier()
+    inp.view[...] = loc
+    inp.to_device()
+    out.view[...] = 0.0
+    out.to_device()
+    dist.barrier()
+    for _ in range(2):
+        gr.launch()
+    native.synchronize(step.compute)
+    ok_g = bool(np.array_equal(out.host_array(), want))
+    if os.environ.get("PEER_DEBUG"):
+        have = inp.host_array()
+        full = d.scatter(g, (2, 2))
+        bad = ~((have == full) | (np.isnan(have) & np.isnan(full)))
+        ob = np.argwhere(out.host_array() != want)
+        print(f"DEBUG-G rank {rank} halo bad {int(bad.sum())} out bad {len(ob)} rows {sorted(set(ob[:, 0].tolist()))[:10]}"
+              f" cols {sorted(set(ob[:, 1].tolist()))[:10]}", flush=True)
+    ok = ok and ok_g
+    line = f"rank {rank} grid {grid} local {d.local_domain} steps {steps} bitwise {ok} (graph replay {ok_g})"
     if timing:
         e0, e1 = native.Event(), native.Event()
         dist.barrier()
@@ -71,8 +112,16 @@ def main():
             step()
         e1.record(step.compute)
         native.synchronize(step.compute)
-        ms = e0.elapsed_ms(e1) / 20
-        line += f" ms_per_step {ms:.4f}"
+        line += f" eager_ms_per_step {e0.elapsed_ms(e1) / 20:.4f}"
+        g20 = step.graph(20)
+        g20.launch()
+        native.synchronize(step.compute)
+        dist.barrier()
+        e0.record(step.compute)
+        g20.launch()
+        e1.record(step.compute)
+        native.synchronize(step.compute)
+        line += f" graph_ms_per_step {e0.elapsed_ms(e1) / 20:.4f}"
     step.exchanger.close()
     print(("PEER_OK " if ok else "PEER_FAIL ") + line, flush=True)
     dist.barrier()
