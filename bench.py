@@ -556,7 +556,9 @@ def run_b200(args, dist):
         "scaling": "weak", "vs_baseline": None, "dtype": dtype,
         "data": "synthetic (reference bench generators, seeds 0..R-1)",
         "config": {"workload": CONFIG_TEXT[args.workload], "domain_per_gpu": list(domain),
-                   "parallelism": f"independent column shards x{dist.world}" if dist.world > 1 else "single GPU",
+                   "parallelism": (f"independent column shards x{dist.world}" if dist.world > 1 else "single GPU")
+                   + (" (GTS_BENCH_SHARED_GPU: all ranks share one GPU -- a code-path check, not a scaling number)"
+                      if dist.shared and dist.world > 1 else ""),
                    "l2": f"{r['nsets']} rotating input/output sets of {r['set_mb']:.0f} MB "
                          f"(> 2x the {r['l2_mb']:.0f} MB L2)",
                    "launch": r["launch"]},
