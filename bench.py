@@ -631,6 +631,29 @@ def run_b200(args, dist):
                 "launches_per_step": r2["launches_per_step"],
             }
         extra["hdiff_decomposed"] = decomp_line
+        # BASELINE configs[0]: hdiff 128x128x64 f64, the reference's CPU-runnable
+        # case -- the b200 kernel and the reference gen kernel on the same inputs
+        try:
+            dom1 = (128, 128, 64)
+            st1 = b200.compile_stencil(workloads.source("hdiff", "f64"), "hdiff")
+            r1 = device_timed(st1, "hdiff", "f64", dom1, max(args.steps // 2, 50), args.warmup, dist,
+                              use_graph=not args.no_graph)
+            pts1 = dom1[0] * dom1[1] * dom1[2]
+            alg1 = workloads.algorithmic_bytes("hdiff", dom1, "f64")
+            c1 = {"workload": "horizontal diffusion 128x128x64 float64 (BASELINE configs[0])",
+                  "value": pts1 / (r1["launch_ms_mean"] / 1e3), "unit": "grid-points/s",
+                  "kernel_ms_mean": r1["launch_ms_mean"],
+                  "achieved_gbs": alg1 / (r1["launch_ms_mean"] / 1e3) / 1e9,
+                  "parity": parity_check("hdiff", "f64", r1["sets"])}
+            if not args.no_cpu_baseline:
+                t1 = time_reference("hdiff", "f64", dom1, seconds=3.0, max_calls=2000)
+                if t1:
+                    c1["cpu_reference"] = {"value": pts1 / statistics.median(t1), "unit": "grid-points/s",
+                                           "median_call_ms": statistics.median(t1) * 1e3,
+                                           "cores": host_info()[0], "calls": len(t1)}
+            extra["hdiff_c1"] = c1
+        except Exception as exc:  # pragma: no cover - reported, not fatal
+            extra["hdiff_c1"] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
         try:
             dy = dycore_timed(dist)
             dy["frac"] = dy["achieved_gbs"] / peak
