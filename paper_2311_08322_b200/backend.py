@@ -154,6 +154,9 @@ last_transfer: dict = {"h2d": 0, "d2h": 0, "chunks": 0}
 _events: list = []
 
 
+PIPE_TRACE = None  # a list to collect per-call device spans of the pipelined mirror mode (probes)
+
+
 def _event(i: int):
     while len(_events) <= i:
         _events.append(native.Event())
@@ -228,7 +231,12 @@ class _Pipeline:
     overwrites entirely (storage == domain, every level unconditionally
     assigned) is never uploaded."""
 
-    CHUNK_ROWS = 32
+    # measured on B200 + PCIe Gen5 (tools/e2e_probe.py, 256^2x80, 3 repeats):
+    # vadv 3.65 / 3.79 / 3.62 / 3.67 ms and hdiff 1.55 / 1.48 / 1.38 / 1.42 ms
+    # per call at 16 / 32 / 64 / 128 rows; a concurrent 2-D device->host copy
+    # slows the host->device stream (0.4 ms at 32 rows), less so with fewer,
+    # larger segments
+    CHUNK_ROWS = 64
 
     def __init__(self, module, impl):
         self.module, self.impl = module, impl
@@ -262,6 +270,8 @@ class _Pipeline:
         ni, nj, nk = domain
         comp = native.default_stream()
         up, down = native.aux_stream("h2d"), native.aux_stream("d2h")
+        if PIPE_TRACE is not None:
+            _event(1000).record(up)
         mirrors, ptrs, strides, origins = {}, {}, {}, {}
         for n in self.module.field_order:
             st, org = field_args[n]
@@ -319,9 +329,17 @@ class _Pipeline:
             for n in self.outputs:
                 o = origins[n][0]
                 d2h += copy(n, o + c0, o + c1, "d2h", down)
+        if PIPE_TRACE is not None:
+            _event(1001).record(up)
+            _event(1002).record(comp)
+            _event(1003).record(down)
         native.synchronize(down)
         native.synchronize(comp)
         last_transfer.update(h2d=h2d, d2h=d2h, chunks=nch)
+        if PIPE_TRACE is not None:
+            t0 = _event(1000)
+            PIPE_TRACE.append({"h2d_ms": t0.elapsed_ms(_event(1001)), "kernels_ms": t0.elapsed_ms(_event(1002)),
+                               "d2h_ms": t0.elapsed_ms(_event(1003))})
 
 
 def build(impl, fp, cache: Optional[BuildCache] = None, options: Optional[dict] = None):
