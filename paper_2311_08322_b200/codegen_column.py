@@ -33,7 +33,7 @@ from dataclasses import dataclass, field
 from typing import Optional
 
 from ._host import ir
-from .codegen import DivPool, _bound, _interval_groups, _MemCtx, c_float, emit_expr  # noqa: F401
+from .codegen import DivPool, _bound, _interval_groups, _MemCtx, c_float, emit_cond, emit_expr  # noqa: F401
 from . import codegen_prologue
 from .lowering import always_writes, reads, writes
 
@@ -265,7 +265,7 @@ def _emit_stmt(stmt, ctx: _Ctx, ctype, api: set, indent: str, out: list) -> None
         pool.invalidate(name)
         return
     if isinstance(stmt, ir.If):
-        cond = emit_expr(stmt.cond, ctx)
+        cond = emit_cond(stmt.cond, ctx)
         pool.flush(indent, out)
         out.append(f"{indent}if ({cond}) {{")
         pool.depth += 1

@@ -27,7 +27,7 @@ from __future__ import annotations
 from dataclasses import dataclass, field
 
 from ._host import ir
-from .codegen import c_float, emit_expr
+from .codegen import c_float, emit_cond, emit_expr  # noqa: F401
 from .lowering import always_writes, reads, writes
 
 Off = tuple  # (di, dj)
@@ -211,7 +211,7 @@ def _emit_stmt(stmt, ctx, ctype: dict, out: list, indent: str) -> None:
         out.append(f"{indent}{ctx.target(name)} = (double)({ctype[name]})({value});")
         return
     if isinstance(stmt, ir.If):
-        out.append(f"{indent}if ({emit_expr(stmt.cond, ctx)}) {{")
+        out.append(f"{indent}if ({emit_cond(stmt.cond, ctx)}) {{")
         for s in stmt.then_body:
             _emit_stmt(s, ctx, ctype, out, indent + "  ")
         if stmt.else_body:
