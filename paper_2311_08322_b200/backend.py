@@ -238,6 +238,28 @@ class _Pipeline:
     # larger segments
     CHUNK_ROWS = 64
 
+    # shrink the last chunks (shorter kernel + D2H tail after the last upload):
+    # measured vadv 256^2x80 3.62 -> 3.58 ms per call, hdiff unchanged (1.37)
+    TAPER = True
+
+    @classmethod
+    def chunk_bounds(cls, ni: int) -> list:
+        """i-row chunks: CHUNK_ROWS each, the last two chunks' worth split
+        into halving pieces (>= 16 rows) when TAPER is on."""
+        c = cls.CHUNK_ROWS
+        if not cls.TAPER:
+            nch = max(1, ni // c)
+            return [(k * ni // nch, (k + 1) * ni // nch) for k in range(nch)]
+        out, r0 = [], 0
+        while r0 < ni:
+            rem = ni - r0
+            n = c if rem > 2 * c else max(16, rem // 2)
+            if rem - n < 16:
+                n = rem
+            out.append((r0, r0 + n))
+            r0 += n
+        return out
+
     def __init__(self, module, impl):
         self.module, self.impl = module, impl
         reads_ = set()
@@ -283,8 +305,8 @@ class _Pipeline:
         skip = {n for n in self.outputs
                 if tuple(field_args[n][0].shape) == tuple(domain) and origins[n] == (0, 0, 0)
                 and _fully_written(self.impl, n, nk)}
-        nch = max(1, ni // self.CHUNK_ROWS)
-        bounds = [(c * ni // nch, (c + 1) * ni // nch) for c in range(nch)]
+        bounds = self.chunk_bounds(ni)
+        nch = len(bounds)
         done_row = {n: 0 for n in self.module.field_order}  # storage rows uploaded so far
         h2d = d2h = 0
 
