@@ -1,0 +1,74 @@
+"""Small runs of every kernel template for compute-sanitizer
+(memcheck / racecheck / synccheck / initcheck), checked against the oracle:
+
+    compute-sanitizer --tool memcheck python tools/sanitize_run.py
+
+Fused PARALLEL tile kernel (hdiff f64 / f32), TMEM column kernels (vadv: W=2
+at nk=20, W=1 at nk=120, generic column kernel at nk=200), the fused dycore
+column kernel, per-stage / plane fallbacks (fuse_parallel off), halo pack /
+unpack and the peer copy-box kernel."""
+import sys
+from pathlib import Path
+
+REPO = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(REPO))
+sys.path.insert(0, str(REPO / "oracle"))
+
+import numpy as np  # noqa: E402
+
+import oracle  # noqa: E402
+import paper_2311_08322_b200 as b200  # noqa: E402
+from paper_2311_08322_b200 import native, workloads  # noqa: E402
+
+rng = np.random.default_rng(5)
+ok = True
+
+
+def check(name, got, want):
+    global ok
+    good = np.array_equal(got, want)
+    ok = ok and good
+    print(f"{name}: {'bitwise' if good else 'MISMATCH'}", flush=True)
+
+
+for dt, npt in (("f64", np.float64), ("f32", np.float32)):
+    vals = rng.uniform(-1, 1, (37 + 4, 70 + 4, 3)).astype(npt)
+    for opts in (None, {"fuse_parallel": False}):
+        st = b200.compile_stencil(workloads.source("hdiff", dt), "hdiff", gen_options=opts)
+        inp = b200.from_array(vals, (2, 2, 0))
+        out = b200.allocate(dt, (37, 70, 3))
+        st(inp=inp, coeff=0.05, out=out)
+        check(f"hdiff {dt} {opts}", out.host_array(), oracle.hdiff_c(vals, 0.05))
+
+for shape in ((19, 40, 20), (9, 33, 120), (5, 6, 200)):
+    a, b, c, d = oracle.make_diagonally_dominant(rng, shape)
+    sv = b200.compile_stencil(workloads.source("vadv"), "vadv")
+    fa = {n: b200.from_array(v) for n, v in zip("abcd", (a, b, c, d))}
+    x = b200.allocate("f64", shape)
+    sv(x=x, **fa)
+    check(f"vadv {shape}", x.host_array(), oracle.vadv_c(a, b, c, d))
+
+ddom = (20, 40, 12)
+arr = workloads.dycore_arrays(ddom, 3)
+sd = b200.compile_stencil(workloads.source("dycore"), "dycore")
+u_in, u_out = b200.from_array(arr["u"], (2, 2, 0)), b200.from_array(arr["u"], (2, 2, 0))
+sd(u_in=u_in, u_out=u_out, **{n: b200.from_array(arr[n]) for n in "abc"}, **workloads.DYCORE_SCALARS)
+check("dycore", u_out.host_array()[2:-2, 2:-2, :],
+      oracle.dycore_step(arr["u"], arr["a"], arr["b"], arr["c"], **workloads.DYCORE_SCALARS))
+
+# halo pack / unpack and the peer copy-box kernel on one device
+f = b200.from_array(rng.uniform(-1, 1, (12, 9, 4)), (2, 2, 0))
+g = b200.allocate("f64", (8, 5, 4), (2, 2, 0))
+s = native.default_stream()
+buf = b200.allocate("f64", (2 * 9 * 4, 1, 1))
+args = [*f.strides, 0, 0, 0, 2, 9, 4, 8, s]
+native.call("gts_b200_pack_box", buf.base_address(), f.base_address(), *args)
+native.call("gts_b200_unpack_box", g.base_address(), buf.base_address(), *[*g.strides, 10, 0, 0, 2, 9, 4, 8, s])
+native.call("gts_b200_copy_box", g.base_address(), *g.strides, f.base_address() + 8 * 2 * f.strides[0],
+            *f.strides, 2, 9, 4, 8, s)
+native.synchronize(s)
+g.mark_device_written()
+fv, gv = f.host_array(), g.host_array()
+check("pack/unpack + copy_box", np.concatenate([gv[:2], gv[10:12]]), np.concatenate([fv[2:4], fv[0:2]]))
+print("SANITIZE_RUN_OK" if ok else "SANITIZE_RUN_FAIL", flush=True)
+sys.exit(0 if ok else 1)
