@@ -20,6 +20,7 @@ work unmodified.
 
 from __future__ import annotations
 
+from dataclasses import dataclass
 from typing import Optional, Union
 
 from . import backend as b200_backend
@@ -55,6 +56,46 @@ def _select_definition(source: str, stencil_name: Optional[str], externals: dict
         raise CompilationError([exc.as_diagnostic()])
 
 
+@dataclass(frozen=True)
+class B200ExecutionReport(sf_runtime.ExecutionReport):
+    """The reference's ExecutionReport (runtime.py:21-38) plus device time:
+    ``device_ns`` = CUDA-event span of the call on the device (host copies
+    included in mirror mode), ``kernel_device_ns`` = the stencil launch alone
+    (None when it interleaves with copies), and the bytes moved each way."""
+
+    device_ns: Optional[int] = None
+    kernel_device_ns: Optional[int] = None
+    h2d_bytes: int = 0
+    d2h_bytes: int = 0
+
+    def as_dict(self) -> dict:
+        d = super().as_dict()
+        d.update(device_ns=self.device_ns, kernel_device_ns=self.kernel_device_ns,
+                 h2d_bytes=self.h2d_bytes, d2h_bytes=self.d2h_bytes)
+        return d
+
+
+@dataclass
+class B200CompiledStencil(sf_runtime.CompiledStencil):
+    """The reference's CompiledStencil; calls return a B200ExecutionReport.
+    ``time_device`` (or GTS_B200_DEVICE_TIME=1) adds CUDA-event device times
+    to the report at ~20 us per call; the byte counts are always there."""
+
+    time_device: bool = False
+
+    def __call__(self, *, domain=None, origin=None, validate=None, **arguments):
+        prev = b200_backend.TIME_DEVICE
+        b200_backend.TIME_DEVICE = prev or self.time_device
+        try:
+            rep = super().__call__(domain=domain, origin=origin, validate=validate, **arguments)
+        finally:
+            b200_backend.TIME_DEVICE = prev
+        t = b200_backend.last_transfer
+        return B200ExecutionReport(rep.total_ns, rep.validate_ns, rep.kernel_ns, rep.domain, rep.validated,
+                                   t.get("device_ns"), t.get("kernel_device_ns"), int(t.get("h2d", 0)),
+                                   int(t.get("d2h", 0)))
+
+
 def compile_stencil(
     source: str,
     stencil_name: Optional[str] = None,
@@ -75,7 +116,7 @@ def compile_stencil(
     fp = ir.fingerprint(bound, BACKEND_ID, externals, toolchain_version(), gen_options)
     cache = BuildCache(cache_dir) if cache_dir is not None else BuildCache()
     executable = b200_backend.build(impl, fp, cache, gen_options)
-    return sf_runtime.CompiledStencil(
+    return B200CompiledStencil(
         name=impl.name,
         fingerprint=fp,
         backend=BACKEND_ID,
@@ -114,4 +155,4 @@ def install() -> None:
     _installed = True
 
 
-__all__ = ["compile_stencil", "install", "InvocationError"]
+__all__ = ["B200CompiledStencil", "B200ExecutionReport", "compile_stencil", "install", "InvocationError"]

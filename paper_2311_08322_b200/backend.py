@@ -19,6 +19,7 @@ fields are mutated in place and the call is synchronous (the runtime times it,
 from __future__ import annotations
 
 import ctypes
+import os
 import weakref
 from typing import Optional
 
@@ -150,7 +151,15 @@ class Module:
 
 
 # bytes moved by the last mirror-mode call (bench.py's e2e line reports them)
-last_transfer: dict = {"h2d": 0, "d2h": 0, "chunks": 0}
+# what the last run() moved and how long the device took (B200ExecutionReport):
+# device_ns = first host->device copy .. last device->host copy (or the launch
+# alone for device storages), kernel_ns = the stencil launches only (None when
+# they interleave with copies in the pipelined mirror mode)
+last_transfer: dict = {"h2d": 0, "d2h": 0, "chunks": 0, "device_ns": None, "kernel_device_ns": None}
+# CUDA-event device timing of run() (4 event records + 2 queries, ~20 us per
+# call from Python, so opt-in: B200CompiledStencil.time_device or the
+# GTS_B200_DEVICE_TIME=1 environment variable)
+TIME_DEVICE = os.environ.get("GTS_B200_DEVICE_TIME") == "1"
 _events: list = []
 
 
@@ -292,7 +301,8 @@ class _Pipeline:
         ni, nj, nk = domain
         comp = native.default_stream()
         up, down = native.aux_stream("h2d"), native.aux_stream("d2h")
-        if PIPE_TRACE is not None:
+        timed = TIME_DEVICE or PIPE_TRACE is not None
+        if timed:
             _event(1000).record(up)
         mirrors, ptrs, strides, origins = {}, {}, {}, {}
         for n in self.module.field_order:
@@ -351,13 +361,17 @@ class _Pipeline:
             for n in self.outputs:
                 o = origins[n][0]
                 d2h += copy(n, o + c0, o + c1, "d2h", down)
-        if PIPE_TRACE is not None:
+        if timed:
             _event(1001).record(up)
             _event(1002).record(comp)
             _event(1003).record(down)
         native.synchronize(down)
         native.synchronize(comp)
         last_transfer.update(h2d=h2d, d2h=d2h, chunks=nch)
+        if timed:
+            t0 = _event(1000)
+            span = max(t0.elapsed_ms(_event(1002)), t0.elapsed_ms(_event(1003)))
+            last_transfer.update(device_ns=int(span * 1e6))
         if PIPE_TRACE is not None:
             t0 = _event(1000)
             PIPE_TRACE.append({"h2d_ms": t0.elapsed_ms(_event(1001)), "kernels_ms": t0.elapsed_ms(_event(1002)),
@@ -411,14 +425,22 @@ def build(impl, fp, cache: Optional[BuildCache] = None, options: Optional[dict] 
     pipe = _Pipeline(module, impl)
 
     def run(domain, field_args, scalar_args) -> None:
+        last_transfer.update(h2d=0, d2h=0, chunks=0, device_ns=None, kernel_device_ns=None)
         if any(d == 0 for d in domain):
             return
         if pipe.eligible(domain, field_args):
             pipe.run(domain, field_args, scalar_args)
             return
         stream = native.default_stream()
+        timed = TIME_DEVICE
+        if timed:
+            _event(2000).record(stream)
         pointers, strides, origins, mirrors = prepare(field_args, stream)
+        if timed:
+            _event(2001).record(stream)
         module.launch(domain, pointers, strides, origins, scalar_args, stream)
+        if timed:
+            _event(2002).record(stream)
         last_transfer.update(h2d=sum(m.nbytes for m, _ in mirrors.values()), d2h=0, chunks=0)
         copied = set()
         for name in module.written:
@@ -433,7 +455,12 @@ def build(impl, fp, cache: Optional[BuildCache] = None, options: Optional[dict] 
                 m = mirrors[key][0]
                 native.call("gts_b200_memcpy_d2h", m.host_base, m.dptr, m.nbytes, stream)
                 last_transfer["d2h"] += m.nbytes
+        if timed:
+            _event(2003).record(stream)
         native.synchronize(stream)
+        if timed:
+            last_transfer.update(device_ns=int(_event(2000).elapsed_ms(_event(2003)) * 1e6),
+                                 kernel_device_ns=int(_event(2001).elapsed_ms(_event(2002)) * 1e6))
 
     build_info = {
         "cache_hit": cache_hit,
