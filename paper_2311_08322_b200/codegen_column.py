@@ -333,7 +333,7 @@ class Variant:
     mat_half: int = 0  # bytes of one set
 
 
-def variants(sp: ThomasSpec, dtypes: dict) -> list:
+def variants(sp: ThomasSpec, dtypes: dict, geoms_override=None) -> list:
     esize = {f: (8 if dtypes[f] == ir.F64 else 4) for f in sp.streamed}
     hist_bytes = 4 * sp.w_level  # bytes per level per column
     out = []
@@ -345,6 +345,8 @@ def variants(sp: ThomasSpec, dtypes: dict) -> list:
     geoms = ((2, 4, 160 * 1024), (2, 4, 128 * 1024), (1, 8, RING_BUDGET))
     if not sp.deep_ring:
         geoms = geoms[1:]
+    if geoms_override:  # gen_options tmem_geom: [[w, kb, ring KiB], ...] (experiments)
+        geoms = tuple((int(w), int(kb), int(kib) * 1024) for w, kb, kib in geoms_override)
     for w, kb, budget in geoms:
         rows = 4 * w
         offs, sb = {}, 0
@@ -406,7 +408,7 @@ def emit(kname: str, plan, kplan, sp: ThomasSpec, ctype: dict, dtypes: dict, opt
     # measured: the deeper ring helps the fused dycore kernel (181 -> 177 us/step)
     # and costs vadv ~0.9 us at 256^2, so it defaults on with a prologue only
     sp.deep_ring = bool((opts or {}).get("deep_ring", sp.pro is not None))
-    for v in variants(sp, dtypes):
+    for v in variants(sp, dtypes, (opts or {}).get("tmem_geom")):
         if only_w and v.w != int(only_w):
             continue
         c, cond, call = _emit_variant(kname, plan, sp, v, ctype, dtypes, opts)
