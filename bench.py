@@ -66,6 +66,8 @@ def parse():
     p.add_argument("--no-extra", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-graph", action="store_true", help="eager launches in the timed loop")
+    p.add_argument("--extra-timeout", type=float, default=420.0,
+                   help="seconds the extra workloads may take before the headline line is printed without them")
     return p.parse_args()
 
 
@@ -576,6 +578,20 @@ def run_b200(args, dist):
                      "peak_source": peak_src, "frac_of_8TBs_spec": achieved / 8000.0},
         "clocks": sampler.summary(),
     }
+    # Watchdog for the extras (multi-rank exchanges that have not run on this
+    # pool's hardware): if they have not finished in time, rank 0 prints the
+    # headline line with the extras marked and every rank exits cleanly, so a
+    # hung collective cannot cost the headline measurement.
+    done = threading.Event()
+
+    def _watchdog():
+        if not done.wait(args.extra_timeout):
+            if dist.rank == 0:
+                line["extra"] = {"error": f"extras timed out after {args.extra_timeout:.0f} s"}
+                print(json.dumps(line), flush=True)
+            os._exit(0)
+
+    threading.Thread(target=_watchdog, daemon=True).start()
     decomp_line = None
     if dist.shared and dist.world > 1:
         decomp_line = {"skipped": "GTS_BENCH_SHARED_GPU: NCCL cannot run two ranks on one GPU"}
@@ -675,8 +691,9 @@ def run_b200(args, dist):
                 "min_call_ms": min(times) * 1e3, "median_call_ms": statistics.median(times) * 1e3,
             }
             line["cpu_baseline"]["rows"] = cpu_rows(kernel, dtype, domain, cores)
+    done.set()
     if dist.rank == 0:
-        print(json.dumps(line))
+        print(json.dumps(line), flush=True)
 
 
 def main():
