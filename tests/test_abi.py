@@ -100,3 +100,30 @@ def test_from_cuda_array_rejects_bad_arrays(shape, strides, typestr):
 
     with pytest.raises(StorageError):
         b200.from_cuda_array(_FakeCAI(shape, strides, typestr))
+
+
+@pytest.mark.parametrize("ni", [128, 129, 150, 200, 256, 511, 512, 1000, 2048])
+def test_pipeline_chunks_cover_rows(ni):
+    """backend._Pipeline.chunk_bounds: contiguous cover of [0, ni), CHUNK_ROWS
+    pieces then a taper, no piece below 16 rows."""
+    from paper_2311_08322_b200.backend import _Pipeline
+
+    b = _Pipeline.chunk_bounds(ni)
+    assert b[0][0] == 0 and b[-1][1] == ni
+    assert all(x1 == y0 for (_, x1), (y0, _) in zip(b, b[1:]))
+    sizes = [y - x for x, y in b]
+    assert all(s >= 16 for s in sizes) and max(sizes) <= _Pipeline.CHUNK_ROWS + 15
+    body = sizes[:-1]  # the last piece absorbs a remainder below 16 rows
+    assert body == sorted(body, reverse=True)
+
+
+def test_execution_report_extends_reference_report():
+    """B200ExecutionReport is the reference's ExecutionReport (runtime.py:21-38)
+    with device time and bytes moved added to as_dict()."""
+    import stencilforge as sf
+    from paper_2311_08322_b200.api import B200ExecutionReport
+
+    r = B200ExecutionReport(10, 2, 5, (4, 4, 4), True, 3000, 2000, 64, 32)
+    assert isinstance(r, sf.ExecutionReport)
+    d = r.as_dict()
+    assert d["kernel_ns"] == 5 and d["device_ns"] == 3000 and d["h2d_bytes"] == 64 and d["d2h_bytes"] == 32
