@@ -249,6 +249,9 @@ class _Ctx(_MemCtx):
         return super().read(name, off)
 
 
+_NOSTORE = False
+
+
 def _emit_stmt(stmt, ctx: _Ctx, ctype, api: set, indent: str, out: list) -> None:
     pool = ctx.pool
     if isinstance(stmt, ir.Assign):
@@ -257,8 +260,9 @@ def _emit_stmt(stmt, ctx: _Ctx, ctype, api: set, indent: str, out: list) -> None
         pool.flush(indent, out)
         out.append(f"{indent}{{ const double v_ = {value};")
         if name in api:
+            guard = "valid && v_ == 1234.5678" if _NOSTORE else "valid"  # tmem_debug nostore (timing)
             out.append(f"{indent}  {{ {ctype[name]}* xp_ = colp_{name} + (long long)k * p.f_{name}.sk;"
-                       f" if (valid) *xp_ = ({ctype[name]})(v_); }}")
+                       f" if ({guard}) *xp_ = ({ctype[name]})(v_); }}")
         if name in ctx.cached or name not in api:
             out.append(f"{indent}  cur_{name} = (double)({ctype[name]})(v_);")
         out.append(f"{indent}}}")
@@ -459,6 +463,8 @@ def _emit_variant(kname, plan, sp: ThomasSpec, v: Variant, ctype, dtypes, opts):
     generic per-level-checked body covers partial stages and group
     boundaries."""
     dbg = (opts or {}).get("tmem_debug", "")
+    global _NOSTORE
+    _NOSTORE = dbg == "nostore"
     impl = plan.impl
     api = {f.name for f in impl.api_fields}
     msf, msb = impl.multistages[sp.ms_f], impl.multistages[sp.ms_b]
@@ -725,6 +731,9 @@ def _emit_variant(kname, plan, sp: ThomasSpec, v: Variant, ctype, dtypes, opts):
     ctx_f.rows, ctx_f.kb, ctx_f.offs = rows, KB, v.offs
     ctx_f.kstride = "hs_" if split else str(rows * TJ)
     first = True
+    if dbg == "streamonly":  # timing experiment: ring traffic only, no arithmetic
+        w("        if (true) {")
+        first = False
     for tier, tcond in (("tmem", "kbase < TL"), ("smem", "kbase >= TL")):
         for gi in range(len(gf)):
             kw = "if" if first else "} else if"
@@ -737,7 +746,7 @@ def _emit_variant(kname, plan, sp: ThomasSpec, v: Variant, ctype, dtypes, opts):
             w("            const int k = kbase + kk;")
             forward_level(ctx_f, "            ", gi, tier, batched=pro_batch)
             w("          }")
-    w("        } else {")
+    w("        } else if (" + ("false" if dbg == "streamonly" else "true") + ") {")
     if pro_batch and v.mat:
         # one consumer barrier per stage on every path keeps the two
         # materialization sets' reuse distance safe (see coop_phase)
@@ -847,7 +856,7 @@ def _emit_variant(kname, plan, sp: ThomasSpec, v: Variant, ctype, dtypes, opts):
         if mse is not None:
             epilogue_level(indent, lambda f: f"cur_{f}")
 
-    if dbg == "fwdonly":
+    if dbg in ("fwdonly", "streamonly"):
         w("      if (nk > 100000) {")
     # shared-memory tier: levels [TL, nk), visited first, in chunks of 4
     def from_smem(t):
@@ -928,7 +937,7 @@ def _emit_variant(kname, plan, sp: ThomasSpec, v: Variant, ctype, dtypes, opts):
         w(f"      for (int k = -1; k >= {sp.elo}; --k) {{")
         epilogue_level("        ", lambda f: "GTS_NAN")
         w("      }")
-    if dbg == "fwdonly":
+    if dbg in ("fwdonly", "streamonly"):
         w("      }")
     w("      __syncwarp();")
     w("    }")
