@@ -392,6 +392,8 @@ def emit(kname: str, plan, kplan, ctype: dict, dtypes: dict, opts=None):
         w(f"    const bool okc_{c} = (jl + {c}) < nj;")
     # register windows
     f32x = bool((opts or {}).get("f32x", True))
+    # timing experiments: "streamonly" = TMA tiles + barriers only; "nostore" = no output stores
+    pf_debug = (opts or {}).get("pf_debug", "")
     for x in regw:
         w(f"    double w_{x.name}[{x.rhi - x.rlo + 1}][{x.chi - x.clo + 1}];")
         if f32x and ctype[x.name] == "float":
@@ -514,7 +516,7 @@ def emit(kname: str, plan, kplan, ctype: dict, dtypes: dict, opts=None):
         for si, st in enumerate(geo.stages):
             li, hi, lj, hj = geo.ext[si]
             # needed rows for stage s: [ra + li, ra + RI - 1 + hi]; row computed = r + hi
-            if rel + hi < li:
+            if rel + hi < li or pf_debug == "streamonly":
                 continue  # prologue: this stage has nothing to produce yet
             w(f"      {{ // stage {si} at row r + {hi}")
             for col in range(lj, VJ + hj):
@@ -535,11 +537,11 @@ def emit(kname: str, plan, kplan, ctype: dict, dtypes: dict, opts=None):
                 _emit_point(st.body, ctx, ctype, api, out, "          ", local, geo)
                 w("        }")
             w("      }")
-        if rel >= 0:
+        if rel >= 0 and pf_debug != "streamonly":
             # buffered api outputs: one row of VJ values per lane, vector store
             for f in sorted(geo.buffered):
                 e = 8 if dtypes[f] == ir.F64 else 4
-                w(f"      if (r < ni) {{")
+                w(f"      if (r < ni{' && nkr < 0' if pf_debug == 'nostore' else ''}) {{")
                 w(f"        {ctype[f]}* const op = &GTS_AT(p.f_{f}, r, jl, kk);")
                 w(f"        if (jl + {VJ} <= nj && p.f_{f}.sj == 1 && (((uintptr_t)op) & 15) == 0) {{")
                 if e == 8:
