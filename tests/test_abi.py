@@ -127,3 +127,31 @@ def test_execution_report_extends_reference_report():
     assert isinstance(r, sf.ExecutionReport)
     d = r.as_dict()
     assert d["kernel_ns"] == 5 and d["device_ns"] == 3000 and d["h2d_bytes"] == 64 and d["d2h_bytes"] == 32
+
+
+def test_binary32_rewrites_in_generated_source():
+    """codegen.emit_f32*: the f32 hdiff tile kernel computes the flux-limiter
+    sign test with float comparisons and flx / fly as single binary32
+    subtractions; the f64 kernel keeps its binary64 multiply; f32x=False
+    restores the plain form (SURVEY.md 8(a) numerics)."""
+    import re
+
+    def src(dtype, opts=None):
+        st = b200.compile_stencil(workloads.source("hdiff", dtype), "hdiff", gen_options=opts)
+        return Path(st.build_info["source_path"]).read_text()
+
+    s32 = src("f32")
+    assert re.search(r"\(\(\(wf_lap\[\d\]\[\d\] > wf_lap\[\d\]\[\d\]\) && \(wf_inp", s32)
+    assert re.search(r"const float vf_ = \(wf_lap\[\d\]\[\d\] - wf_lap\[\d\]\[\d\]\);", s32)
+    s64 = src("f64")
+    assert "wf_" not in s64 and "> 0x0.0p+0" in s64
+    plain = src("f32", {"f32x": False})
+    assert "wf_" not in plain
+
+
+def test_f32_exact_literals():
+    from paper_2311_08322_b200.codegen import _f32_exact_literal
+
+    assert _f32_exact_literal(0.0) and _f32_exact_literal(4.0) and _f32_exact_literal(-0.5)
+    assert not _f32_exact_literal(0.1) and not _f32_exact_literal(1e300)
+    assert not _f32_exact_literal(float("nan")) and not _f32_exact_literal(float("inf"))
