@@ -151,6 +151,10 @@ def analyse(plan, kplan, dtypes: dict) -> Geo:
     for name, wv in sorted(geo.wins.items()):
         if wv.kind != "stream":
             continue
+        if PREFETCH:
+            # one extra row slot: each step loads the row the NEXT step needs,
+            # so shared-memory load latency overlaps a whole step of arithmetic
+            wv.rhi += PREFETCH
         e = 8 if dtypes[name] == ir.F64 else 4
         wv.esize = e
         align = 16 // e
@@ -281,15 +285,18 @@ def _emit_point(stmt, ctx: _Ctx, ctype, api: set, out: list, indent: str, local:
     raise TypeError(type(stmt).__name__)
 
 
-DEFAULTS = {"pf_nw": 4, "pf_ri": 8, "pf_vj": 4, "pf_nbuf": 1}  # + pf_pdl: off|early|late
+PREFETCH = 0  # gen_options pf_prefetch: stream rows loaded this many steps early
+DEFAULTS = {"pf_nw": 4, "pf_ri": 8, "pf_vj": 4, "pf_nbuf": 1, "pf_prefetch": 0}  # + pf_pdl: off|early|late
 # Measured defaults per element size (profiles/sweep_hdiff_r1.md, hdiff
 # 256x256x80 on one B200, CUDA-graph timed):
 #  f64: 16x128 tiles, double-buffered TMA boxes: 16.9 us vs 18.1 us for
 #       32x128 single-buffered (HBM-bound; shorter tiles shrink the tail);
 #  f32: 16x128 tiles with 2 warps x 8 rows, double-buffered: FP64-pipe bound
 #       (f64 arithmetic on f32 storage), so fewer halo recomputations win.
-GEOMETRY = {8: {"pf_nw": 4, "pf_ri": 4, "pf_vj": 4, "pf_nbuf": 2},
-            4: {"pf_nw": 2, "pf_ri": 8, "pf_vj": 4, "pf_nbuf": 2}}
+#  pf_prefetch (rows loaded one step early): f32 15.68 -> 15.12 us; f64 16.99 ->
+#       16.79 us at 256^2 but 112.3 -> 116.6 us at 512x1024, so f32 only.
+GEOMETRY = {8: {"pf_nw": 4, "pf_ri": 4, "pf_vj": 4, "pf_nbuf": 2, "pf_prefetch": 0},
+            4: {"pf_nw": 2, "pf_ri": 8, "pf_vj": 4, "pf_nbuf": 2, "pf_prefetch": 1}}
 
 
 def configure(opts, esize: int = 0) -> None:
@@ -297,10 +304,11 @@ def configure(opts, esize: int = 0) -> None:
     fingerprint like the reference gen engine's tile options, gen.py:235-238).
     Unset options take the measured default of the group's smallest streamed
     element size ``esize`` (0: the generic DEFAULTS)."""
-    global NW, RI, VJ, TJ, TI, NBUF
+    global NW, RI, VJ, TJ, TI, NBUF, PREFETCH
     o = dict(GEOMETRY.get(esize, DEFAULTS))
     o.update({k: v for k, v in (opts or {}).items() if k in DEFAULTS})
     NW, RI, VJ, NBUF = int(o["pf_nw"]), int(o["pf_ri"]), int(o["pf_vj"]), int(o["pf_nbuf"])
+    PREFETCH = int(o["pf_prefetch"])
     TJ, TI = 32 * VJ, NW * RI
 
 
