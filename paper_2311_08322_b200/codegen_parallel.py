@@ -286,17 +286,20 @@ def _emit_point(stmt, ctx: _Ctx, ctype, api: set, out: list, indent: str, local:
 
 
 PREFETCH = 0  # gen_options pf_prefetch: stream rows loaded this many steps early
-DEFAULTS = {"pf_nw": 4, "pf_ri": 8, "pf_vj": 4, "pf_nbuf": 1, "pf_prefetch": 0}  # + pf_pdl: off|early|late
+SWZ = False  # gen_options pf_swz: lane-alternating paired row loads (bank spreading)
+DEFAULTS = {"pf_nw": 4, "pf_ri": 8, "pf_vj": 4, "pf_nbuf": 1, "pf_prefetch": 0, "pf_swz": 0}  # + pf_pdl: off|early|late
 # Measured defaults per element size (profiles/sweep_hdiff_r1.md, hdiff
 # 256x256x80 on one B200, CUDA-graph timed):
 #  f64: 16x128 tiles, double-buffered TMA boxes: 16.9 us vs 18.1 us for
 #       32x128 single-buffered (HBM-bound; shorter tiles shrink the tail);
 #  f32: 16x128 tiles with 2 warps x 8 rows, double-buffered: FP64-pipe bound
 #       (f64 arithmetic on f32 storage), so fewer halo recomputations win.
-#  pf_prefetch (rows loaded one step early): f32 15.68 -> 15.12 us; f64 16.99 ->
-#       16.79 us at 256^2 but 112.3 -> 116.6 us at 512x1024, so f32 only.
-GEOMETRY = {8: {"pf_nw": 4, "pf_ri": 4, "pf_vj": 4, "pf_nbuf": 2, "pf_prefetch": 0},
-            4: {"pf_nw": 2, "pf_ri": 8, "pf_vj": 4, "pf_nbuf": 2, "pf_prefetch": 1}}
+#  pf_prefetch (rows loaded one step early) + pf_swz (bank-spread row loads):
+#       interleaved A/B (tools/abtest.py, medians of 5): f64 256^2 17.00 -> 16.59 us,
+#       512x1024 112.3 -> 113.0 us (noise); f32 prefetch alone 15.68 -> 15.12 us
+#       (f32 with pf_swz: 17.6 us, so not for f32).
+GEOMETRY = {8: {"pf_nw": 4, "pf_ri": 4, "pf_vj": 4, "pf_nbuf": 2, "pf_prefetch": 1, "pf_swz": 1},
+            4: {"pf_nw": 2, "pf_ri": 8, "pf_vj": 4, "pf_nbuf": 2, "pf_prefetch": 1, "pf_swz": 0}}
 
 
 def configure(opts, esize: int = 0) -> None:
@@ -304,11 +307,12 @@ def configure(opts, esize: int = 0) -> None:
     fingerprint like the reference gen engine's tile options, gen.py:235-238).
     Unset options take the measured default of the group's smallest streamed
     element size ``esize`` (0: the generic DEFAULTS)."""
-    global NW, RI, VJ, TJ, TI, NBUF, PREFETCH
+    global NW, RI, VJ, TJ, TI, NBUF, PREFETCH, SWZ
     o = dict(GEOMETRY.get(esize, DEFAULTS))
     o.update({k: v for k, v in (opts or {}).items() if k in DEFAULTS})
     NW, RI, VJ, NBUF = int(o["pf_nw"]), int(o["pf_ri"]), int(o["pf_vj"]), int(o["pf_nbuf"])
     PREFETCH = int(o["pf_prefetch"])
+    SWZ = bool(int(o["pf_swz"]))
     TJ, TI = 32 * VJ, NW * RI
 
 
@@ -422,15 +426,15 @@ def emit(kname: str, plan, kplan, ctype: dict, dtypes: dict, opts=None):
     # the LDS bandwidth).  Chunks are loaded in pairs whose offsets differ by
     # V..S-V (mod S): lane groups alternate which one they load first, so one
     # instruction covers all 32 banks; selects put the values back in place.
-    # Measured (tools/ksweep.py, B200): hdiff f64 256^2x80 17.11 -> 16.77 us,
-    # but 512x1024x80 113.1 -> 116.1 us and f32 256^2 15.65 -> 16.49 us (the
-    # selects cost more than the halved wavefronts save), so it is opt-in.
+    # Measured alone (tools/ksweep.py): f64 256^2 17.11 -> 16.77 us, 512x1024
+    # 113.1 -> 116.1 us, f32 slower; with pf_prefetch it is the f64 default
+    # (GEOMETRY above).
     lane_stride = {s.name: VJ * s.esize for s in streams}
     swz = {}
     for s in streams:
         S = lane_stride[s.name]
         g = 128 // S if S and 128 % S == 0 else 0
-        if bool((opts or {}).get("pf_swz", False)) and g >= 1 and (g & (g - 1)) == 0 and 1 < g <= 16:
+        if SWZ and g >= 1 and (g & (g - 1)) == 0 and 1 < g <= 16:
             swz[s.name] = g
     for g in sorted(set(swz.values())):
         w(f"    const int swz{g}_ = (lane / {g}) & 1;")
