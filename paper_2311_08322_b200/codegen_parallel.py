@@ -298,7 +298,10 @@ DEFAULTS = {"pf_nw": 4, "pf_ri": 8, "pf_vj": 4, "pf_nbuf": 1, "pf_prefetch": 0, 
 #       interleaved A/B (tools/abtest.py, medians of 5): f64 256^2 17.00 -> 16.59 us,
 #       512x1024 112.3 -> 113.0 us (noise); f32 prefetch alone 15.68 -> 15.12 us
 #       (f32 with pf_swz: 17.6 us, so not for f32).
-GEOMETRY = {8: {"pf_nw": 4, "pf_ri": 4, "pf_vj": 4, "pf_nbuf": 2, "pf_prefetch": 1, "pf_swz": 1},
+#  f64 then 2 warps per CTA (8x128 tiles): 16.52 -> 16.07 us at 256^2, 112.6 -> 112.1
+#       at 512x1024 (tools/abtest.py); 1 or 3 warps, 6- or 8-row strips, 1 or 3
+#       buffers all measured slower.
+GEOMETRY = {8: {"pf_nw": 2, "pf_ri": 4, "pf_vj": 4, "pf_nbuf": 2, "pf_prefetch": 1, "pf_swz": 1},
             4: {"pf_nw": 2, "pf_ri": 8, "pf_vj": 4, "pf_nbuf": 2, "pf_prefetch": 1, "pf_swz": 0}}
 
 
