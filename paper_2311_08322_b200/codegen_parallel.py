@@ -287,7 +287,8 @@ def _emit_point(stmt, ctx: _Ctx, ctype, api: set, out: list, indent: str, local:
 
 PREFETCH = 0  # gen_options pf_prefetch: stream rows loaded this many steps early
 SWZ = False  # gen_options pf_swz: lane-alternating paired row loads (bank spreading)
-DEFAULTS = {"pf_nw": 4, "pf_ri": 8, "pf_vj": 4, "pf_nbuf": 1, "pf_prefetch": 0, "pf_swz": 0}  # + pf_pdl: off|early|late
+PDL = "off"  # gen_options pf_pdl: programmatic dependent launch off | early | late
+DEFAULTS = {"pf_nw": 4, "pf_ri": 8, "pf_vj": 4, "pf_nbuf": 1, "pf_prefetch": 0, "pf_swz": 0, "pf_pdl": "off"}  # + pf_pdl: off|early|late
 # Measured defaults per element size (profiles/sweep_hdiff_r1.md, hdiff
 # 256x256x80 on one B200, CUDA-graph timed):
 #  f64: 16x128 tiles, double-buffered TMA boxes: 16.9 us vs 18.1 us for
@@ -301,8 +302,12 @@ DEFAULTS = {"pf_nw": 4, "pf_ri": 8, "pf_vj": 4, "pf_nbuf": 1, "pf_prefetch": 0, 
 #  f64 then 2 warps per CTA (8x128 tiles): 16.52 -> 16.07 us at 256^2, 112.6 -> 112.1
 #       at 512x1024 (tools/abtest.py); 1 or 3 warps, 6- or 8-row strips, 1 or 3
 #       buffers all measured slower.
-GEOMETRY = {8: {"pf_nw": 2, "pf_ri": 4, "pf_vj": 4, "pf_nbuf": 2, "pf_prefetch": 1, "pf_swz": 1},
-            4: {"pf_nw": 2, "pf_ri": 8, "pf_vj": 4, "pf_nbuf": 2, "pf_prefetch": 1, "pf_swz": 0}}
+#  f64 pf_pdl "late" (dependent launch triggered at each CTA's last tile): 16.14 ->
+#       15.97 us at 256^2, 6.13 -> 5.98 us at 128^2x64; f32 15.15 -> 15.22 (off).
+GEOMETRY = {8: {"pf_nw": 2, "pf_ri": 4, "pf_vj": 4, "pf_nbuf": 2, "pf_prefetch": 1, "pf_swz": 1,
+                "pf_pdl": "late"},
+            4: {"pf_nw": 2, "pf_ri": 8, "pf_vj": 4, "pf_nbuf": 2, "pf_prefetch": 1, "pf_swz": 0,
+                "pf_pdl": "off"}}
 
 
 def configure(opts, esize: int = 0) -> None:
@@ -310,12 +315,13 @@ def configure(opts, esize: int = 0) -> None:
     fingerprint like the reference gen engine's tile options, gen.py:235-238).
     Unset options take the measured default of the group's smallest streamed
     element size ``esize`` (0: the generic DEFAULTS)."""
-    global NW, RI, VJ, TJ, TI, NBUF, PREFETCH, SWZ
+    global NW, RI, VJ, TJ, TI, NBUF, PREFETCH, SWZ, PDL
     o = dict(GEOMETRY.get(esize, DEFAULTS))
     o.update({k: v for k, v in (opts or {}).items() if k in DEFAULTS})
     NW, RI, VJ, NBUF = int(o["pf_nw"]), int(o["pf_ri"]), int(o["pf_vj"]), int(o["pf_nbuf"])
     PREFETCH = int(o["pf_prefetch"])
     SWZ = bool(int(o["pf_swz"]))
+    PDL = str(o["pf_pdl"])
     TJ, TI = 32 * VJ, NW * RI
 
 
@@ -354,7 +360,7 @@ def emit(kname: str, plan, kplan, ctype: dict, dtypes: dict, opts=None):
     w("  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;")
     w(f"  if (threadIdx.x == 0) {{ for (int b = 0; b < {NBUF}; ++b) gts_mbar_init(&full[b], 1); gts_fence_mbar_init(); }}")
     w("  __syncthreads();")
-    pdl = (opts or {}).get("pf_pdl", "off")  # measured: early-trigger PDL slows 256^2 hdiff
+    pdl = PDL  # off | early | late (configure(): per element size, gen_options pf_pdl)
     if pdl == "early":
         w("  gts_griddep_launch_dependents();")
     if pdl != "off":
