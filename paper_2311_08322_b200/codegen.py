@@ -545,12 +545,18 @@ def generate_source(plan: Plan, fp, options: Optional[dict] = None) -> str:
             saved_launches = launches
             if fused_col is not None:
                 launches = []
-            res = None
+            res = resL = None
             if opts.get("tma", True):
                 if opts.get("pf_mode", "tile") == "row":
                     res = codegen_rowstream.emit(kname, plan, k, ctype, dtypes, opts)
                 else:
                     res = codegen_parallel.emit(kname, plan, k, ctype, dtypes, opts)
+                    # binary64 groups: a second geometry for large domains, chosen at
+                    # launch (codegen_parallel.LARGE)
+                    if (res is not None and codegen_parallel.last_esize() == 8 and "pf_nw" not in opts
+                            and opts.get("pf_dual", True)):
+                        resL = codegen_parallel.emit(kname + "L", plan, k, ctype, dtypes,
+                                                     {**opts, **codegen_parallel.LARGE})
             fb = []
             for r in k.stages:
                 nm = f"{kname}_s{r.idx}"
@@ -560,13 +566,24 @@ def generate_source(plan: Plan, fp, options: Optional[dict] = None) -> str:
                 launches += fb
                 for t in k.local_temps:
                     local_of[t] = -1  # always needs its arena slot
-            else:
+            elif resL is None:
                 code, pre, launch = res
                 out.extend(code)
                 flag = f"fz_ok_{kidx}"
                 fused_ok[kidx] = flag
                 prelude += pre
                 launches += [f"  if ({flag}) {{"] + launch + ["  } else {"] + fb + ["  }"]
+            else:
+                code, pre, launch = res
+                codeL, preL, launchL = resL
+                out.extend(code + codeL)
+                flag, flagL = f"fz_ok_{kidx}", f"fz_okL_{kidx}"
+                fused_ok[kidx] = f"({flag} || {flagL})"
+                prelude += pre + [ln.replace(flag, flagL) for ln in preL]
+                prelude.append(f"  const bool fzs_{kidx} = (long long)ni * nj * nk < "
+                               f"{codegen_parallel.LARGE_POINTS}LL;  // small domain: the default geometry")
+                launches += ([f"  if ({flag} && (fzs_{kidx} || !{flagL})) {{"] + launch
+                             + [f"  }} else if ({flagL}) {{"] + launchL + ["  } else {"] + fb + ["  }"])
             if fused_col is not None:
                 pf_lines = launches
                 launches = saved_launches

@@ -310,6 +310,20 @@ GEOMETRY = {8: {"pf_nw": 2, "pf_ri": 4, "pf_vj": 4, "pf_nbuf": 2, "pf_prefetch":
                 "pf_pdl": "off"}}
 
 
+# Large binary64 domains use 4 warps per CTA: in eager launches 512x1024x80 runs
+# 129.4 us with the 2-warp default and 116.4 us with 4 warps (graph replay:
+# 112.5 vs 115.1); at 256^2 the 2-warp geometry wins (graph 16.07 vs 16.52,
+# eager equal).  Domains of >= LARGE_POINTS points launch the LARGE variant.
+LARGE = {"pf_nw": 4}
+LARGE_POINTS = 16 * 1024 * 1024
+_LAST_ESIZE = 0
+
+
+def last_esize() -> int:
+    """Element size the last emit() configured for (8: binary64 group)."""
+    return _LAST_ESIZE
+
+
 def configure(opts, esize: int = 0) -> None:
     """Tile geometry (gen_options pf_nw / pf_ri / pf_vj / pf_nbuf; part of the
     fingerprint like the reference gen engine's tile options, gen.py:235-238).
@@ -333,7 +347,9 @@ def _min_esize(plan, kplan, dtypes: dict) -> int:
 
 
 def emit(kname: str, plan, kplan, ctype: dict, dtypes: dict, opts=None):
-    configure(opts, _min_esize(plan, kplan, dtypes))
+    global _LAST_ESIZE
+    _LAST_ESIZE = _min_esize(plan, kplan, dtypes)
+    configure(opts, _LAST_ESIZE)
     geo = eligible(plan, kplan, dtypes)
     if geo is None:
         return None
