@@ -538,7 +538,8 @@ def _emit_variant(kname, plan, sp: ThomasSpec, v: Variant, ctype, dtypes, opts):
     w("        for (int kb = 0; kb < nkb; ++kb, ++it) {")
     w("          const int s = it % NST;")
     w("          const uint32_t ph = (uint32_t)(it / NST) & 1u;")
-    w("          if (it >= NST) gts_mbar_wait_sleep(&empty[s], ph ^ 1u);")
+    sleep_ns = int((opts or {}).get("col_sleep_ns", 200))  # producer back-off on a full ring
+    w(f"          if (it >= NST) gts_mbar_wait_sleep<{sleep_ns}>(&empty[s], ph ^ 1u);")
     if split:
         w("          gts_mbar_arrive_expect_tx(&full[s], txb_);")
         w("          if (c2_) {")

@@ -61,8 +61,11 @@ __device__ __forceinline__ bool gts_mbar_try(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+template <int kSleepNs = 200>
 __device__ __forceinline__ void gts_mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
-  while (!gts_mbar_try(bar, parity)) __nanosleep(200);
+  while (!gts_mbar_try(bar, parity)) {
+    if (kSleepNs > 0) __nanosleep(kSleepNs);
+  }
 }
 
 // Generic-proxy reads of a smem buffer must be ordered before the async
