@@ -26,6 +26,7 @@ exact hex literals (``gen.py:111-116``).
 from __future__ import annotations
 
 import math
+import threading
 from typing import Optional
 
 from ._host import ir
@@ -459,7 +460,18 @@ def _point_kernel(kname: str, stage, ctype: dict, dtypes: dict) -> list:
 # ---------------------------------------------------------------------------
 
 
+_GEN_LOCK = threading.Lock()
+
+
 def generate_source(plan: Plan, fp, options: Optional[dict] = None) -> str:
+    """One CUDA translation unit for ``plan``.  The template emitters keep
+    their geometry in module state while they run (codegen_parallel.configure
+    and friends), so concurrent callers are serialised."""
+    with _GEN_LOCK:
+        return _generate_source(plan, fp, options)
+
+
+def _generate_source(plan: Plan, fp, options: Optional[dict] = None) -> str:
     impl = plan.impl
     from . import codegen_column, codegen_parallel, codegen_rowstream  # template instantiations
 
