@@ -557,18 +557,20 @@ def _generate_source(plan: Plan, fp, options: Optional[dict] = None) -> str:
             saved_launches = launches
             if fused_col is not None:
                 launches = []
-            res = resL = None
+            res = resL = resT = None
             if opts.get("tma", True):
                 if opts.get("pf_mode", "tile") == "row":
                     res = codegen_rowstream.emit(kname, plan, k, ctype, dtypes, opts)
                 else:
                     res = codegen_parallel.emit(kname, plan, k, ctype, dtypes, opts)
-                    # binary64 groups: a second geometry for large domains, chosen at
-                    # launch (codegen_parallel.LARGE)
+                    # binary64 groups: extra geometries for large and for tiny domains,
+                    # chosen at launch (codegen_parallel.LARGE / TINY)
                     if (res is not None and codegen_parallel.last_esize() == 8 and "pf_nw" not in opts
-                            and opts.get("pf_dual", True)):
+                            and "pf_ri" not in opts and opts.get("pf_dual", True)):
                         resL = codegen_parallel.emit(kname + "L", plan, k, ctype, dtypes,
                                                      {**opts, **codegen_parallel.LARGE})
+                        resT = codegen_parallel.emit(kname + "T", plan, k, ctype, dtypes,
+                                                     {**opts, **codegen_parallel.TINY})
             fb = []
             for r in k.stages:
                 nm = f"{kname}_s{r.idx}"
@@ -590,11 +592,22 @@ def _generate_source(plan: Plan, fp, options: Optional[dict] = None) -> str:
                 codeL, preL, launchL = resL
                 out.extend(code + codeL)
                 flag, flagL = f"fz_ok_{kidx}", f"fz_okL_{kidx}"
-                fused_ok[kidx] = f"({flag} || {flagL})"
                 prelude += pre + [ln.replace(flag, flagL) for ln in preL]
-                prelude.append(f"  const bool fzs_{kidx} = (long long)ni * nj * nk < "
-                               f"{codegen_parallel.LARGE_POINTS}LL;  // small domain: the default geometry")
-                launches += ([f"  if ({flag} && (fzs_{kidx} || !{flagL})) {{"] + launch
+                pts = f"(long long)ni * nj * nk"
+                prelude.append(f"  const bool fzs_{kidx} = {pts} < {codegen_parallel.LARGE_POINTS}LL;"
+                               "  // not large: the default geometry")
+                head = []
+                if resT is not None:
+                    codeT, preT, launchT = resT
+                    out.extend(codeT)
+                    flagT = f"fz_okT_{kidx}"
+                    prelude += [ln.replace(flag, flagT) for ln in preT]
+                    prelude.append(f"  const bool fzt_{kidx} = {pts} < {codegen_parallel.TINY_POINTS}LL;")
+                    fused_ok[kidx] = f"({flag} || {flagL} || {flagT})"
+                    head = [f"  if ({flagT} && fzt_{kidx}) {{"] + launchT + ["  } else"]
+                else:
+                    fused_ok[kidx] = f"({flag} || {flagL})"
+                launches += (head + [f"  if ({flag} && (fzs_{kidx} || !{flagL})) {{"] + launch
                              + [f"  }} else if ({flagL}) {{"] + launchL + ["  } else {"] + fb + ["  }"])
             if fused_col is not None:
                 pf_lines = launches

@@ -316,6 +316,10 @@ GEOMETRY = {8: {"pf_nw": 2, "pf_ri": 4, "pf_vj": 4, "pf_nbuf": 2, "pf_prefetch":
 # eager equal).  Domains of >= LARGE_POINTS points launch the LARGE variant.
 LARGE = {"pf_nw": 4}
 LARGE_POINTS = 16 * 1024 * 1024
+# Tiny binary64 domains (< TINY_POINTS) use 2-row strips: 128^2x64 5.97 -> 5.58 us,
+# but 192^2x80 12.54 -> 14.10 us (tools/abtest.py).
+TINY = {"pf_ri": 2}
+TINY_POINTS = 2 * 1024 * 1024
 _LAST_ESIZE = 0
 
 
