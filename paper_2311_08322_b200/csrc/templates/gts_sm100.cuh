@@ -6,6 +6,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <string.h>
 #include <vector>
 
 // ---------------------------------------------------------------------------
@@ -245,6 +246,31 @@ static bool gts_make_tmap_3d(CUtensorMap* map, const void* origin, int itemsize,
   if (((uintptr_t)origin) % 16) return false;
   if ((s_i * itemsize) % 16 || (s_k * itemsize) % 16) return false;
   if (s_i <= 0 || s_k <= 0) return false;
+  // repeat calls on the same fields reuse the encoded map (a small per-thread
+  // cache keyed by every encoding input): the host cost of a repeated launch
+  struct Key {
+    const void* o;
+    long long v[8];
+    unsigned b[3];
+  };
+  struct Entry {
+    Key k;
+    CUtensorMap m;
+    bool used;
+  };
+  static thread_local Entry cache[16];
+  static thread_local unsigned next_slot = 0;
+  Key key;
+  memset(&key, 0, sizeof(key));
+  key.o = origin;
+  key.v[0] = itemsize, key.v[1] = nj, key.v[2] = ni, key.v[3] = nk;
+  key.v[4] = s_i, key.v[5] = s_j, key.v[6] = s_k;
+  key.b[0] = bj, key.b[1] = bi, key.b[2] = bk;
+  for (int e = 0; e < 16; ++e)
+    if (cache[e].used && memcmp(&cache[e].k, &key, sizeof(key)) == 0) {
+      *map = cache[e].m;
+      return true;
+    }
   cuuint64_t dims[3] = {(cuuint64_t)nj, (cuuint64_t)ni, (cuuint64_t)nk};
   cuuint64_t strides[2] = {(cuuint64_t)(s_i * itemsize), (cuuint64_t)(s_k * itemsize)};
   cuuint32_t box[3] = {bj, bi, bk};
@@ -253,7 +279,12 @@ static bool gts_make_tmap_3d(CUtensorMap* map, const void* origin, int itemsize,
                    3, const_cast<void*>(origin), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS;
+  if (r != CUDA_SUCCESS) return false;
+  Entry& slot = cache[next_slot++ % 16];
+  slot.k = key;
+  slot.m = *map;
+  slot.used = true;
+  return true;
 }
 
 static int gts_sm_count() {
