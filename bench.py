@@ -491,6 +491,49 @@ def decomposed_hdiff(dist, steps, warmup, tile=(512, 1024, 80), transport="nccl"
     return ms, gdom, grid, step.launches_per_step
 
 
+def dycore_decomposed_peer(dist, steps=20, tile=(512, 512, 80)):
+    """The dycore step (configs[4]) weak-scaled: a 512x512x80 tile per GPU on
+    the rank grid, the halo of u_in exchanged by peer stores each step
+    (PeerDecomposedStep, one per u_in / u_out swap), ``steps`` steps replayed
+    from one CUDA graph; max over ranks."""
+    import paper_2311_08322_b200 as b200
+    from paper_2311_08322_b200 import decomp, native, workloads
+
+    grid = decomp.choose_grid(dist.world)
+    gdom = (tile[0] * grid[0], tile[1] * grid[1], tile[2])
+    d = decomp.Decomposition(gdom, grid, dist.rank)
+    arr = workloads.dycore_arrays(d.local_domain, 2000 + dist.rank)  # per-rank synthetic state
+    st = b200.compile_stencil(workloads.source("dycore"), "dycore")
+    A, B = b200.from_array(arr["u"], (2, 2, 0)), b200.from_array(arr["u"], (2, 2, 0))
+    coef = {n: b200.from_array(arr[n]) for n in "abc"}
+    sc = workloads.DYCORE_SCALARS
+    s_ab = decomp.PeerDecomposedStep(st, d, {"u_in": A, "u_out": B, **coef}, sc, "u_in", (2, 2))
+    s_ba = decomp.PeerDecomposedStep(st, d, {"u_in": B, "u_out": A, **coef}, sc, "u_in", (2, 2))
+    for s in range(4):
+        (s_ab if s % 2 == 0 else s_ba)()
+    stream = s_ab.compute
+    native.synchronize(stream)
+    g = native.Graph(stream)
+    with g.capture():
+        for s in range(steps):
+            (s_ab if s % 2 == 0 else s_ba)()
+    g.launch()
+    native.synchronize(stream)
+    e0, e1 = native.Event(), native.Event()
+    dist.barrier()
+    e0.record(stream)
+    g.launch()
+    e1.record(stream)
+    native.synchronize(stream)
+    dist.barrier()
+    ms = dist.max(e0.elapsed_ms(e1) / steps)
+    pts = gdom[0] * gdom[1] * gdom[2]
+    return {"workload": f"dycore step, {tile[0]}x{tile[1]}x{tile[2]} per GPU on a {grid[0]}x{grid[1]} grid "
+                        f"(global {gdom[0]}x{gdom[1]}x{gdom[2]}), u_in halo by peer stores, {steps} steps "
+                        "replayed from one CUDA graph",
+            "value": pts / (ms / 1e3), "unit": "grid-point-steps/s", "ms_per_step": ms, "scaling": "weak"}
+
+
 def dycore_timed(dist, steps=100, domain=(512, 512, 80), reps=3, gen_options=None):
     """BASELINE.json configs[4]: the dycore-like step (kernels/dycore.gts:
     hdiff -> Thomas solve -> interval-specialised update) on 512x512x80 f64,
@@ -637,8 +680,15 @@ def run_b200(args, dist):
             }
         except Exception as exc:  # pragma: no cover - reported, not fatal
             peer_line = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+    dy_peer = None
+    if not args.no_extra and dist.world > 1:
+        try:
+            dy_peer = dycore_decomposed_peer(dist)
+        except Exception as exc:  # pragma: no cover - reported, not fatal
+            dy_peer = {"error": f"{type(exc).__name__}: {exc}"[:300]}
     if dist.rank == 0 and dist.world > 1:
-        line["extra"] = {"hdiff_decomposed": decomp_line, "hdiff_decomposed_peer": peer_line}
+        line["extra"] = {"hdiff_decomposed": decomp_line, "hdiff_decomposed_peer": peer_line,
+                         "dycore_decomposed_peer": dy_peer}
     if dist.rank == 0 and dist.world == 1 and not args.no_extra:
         extra = {}
         for name in ("hdiff", "hdiff32"):

@@ -206,3 +206,20 @@ def test_peer_halo_exchange_multiprocess(world):
     # ranks print concurrently: lines may interleave, so count markers
     assert r.returncode == 0 and r.stdout.count("PEER_OK") == world and "PEER_FAIL" not in r.stdout, (
         r.stdout[-2000:], r.stderr[-3000:])
+
+
+@pytest.mark.gpu
+def test_peer_dycore_decomposed_multiprocess():
+    """The fused dycore step (kernels/dycore.gts) decomposed over 2 processes
+    with the peer-memory exchange of u_in's halo (two PeerDecomposedSteps for
+    the u_in / u_out swap): bitwise the undecomposed oracle after 4 steps."""
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    repo = Path(__file__).resolve().parent.parent
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           str(repo / "tools" / "peer_dycore_check.py"), "4"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=str(repo))
+    assert r.returncode == 0 and r.stdout.count("DYCORE_PEER_OK") == 2, (r.stdout[-2000:], r.stderr[-3000:])
