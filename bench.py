@@ -239,11 +239,42 @@ def time_reference(kernel, dtype, domain, seconds: float, max_calls: int, warmup
     return times
 
 
+def arena_reuse_row(kernel, dtype, domain, seconds=4.0):
+    """the gen kernel with glibc arena reuse.  The generated C
+    allocates its temporary arena per call (gen.py:301-323, 361-362); above
+    the mmap threshold every call maps fresh pages and page-faults them.  The
+    survey's MALLOC_MMAP_THRESHOLD_/MALLOC_TRIM_THRESHOLD_ environment is read
+    at process start, so the same effect is set here with mallopt (no mmap'd
+    chunks, no trimming) for this row only, then restored."""
+    pts = domain[0] * domain[1] * domain[2]
+    try:
+        libc = ctypes.CDLL(None)
+        M_TRIM_THRESHOLD, M_MMAP_MAX = -1, -4
+        if not (libc.mallopt(M_TRIM_THRESHOLD, 2 ** 31 - 1) and libc.mallopt(M_MMAP_MAX, 0)):
+            return {"error": "mallopt refused"}
+        try:
+            t = time_reference(kernel, dtype, domain, seconds=seconds, max_calls=1000, warmup=3)
+        finally:
+            libc.mallopt(M_MMAP_MAX, 65536)
+            libc.mallopt(M_TRIM_THRESHOLD, 128 * 1024)
+    except Exception as exc:  # pragma: no cover - reported, not fatal
+        return {"error": f"{type(exc).__name__}: {exc}"[:200]}
+    if not t:
+        return None
+    return {"value": pts / statistics.median(t), "calls": len(t),
+            "median_call_ms": statistics.median(t) * 1e3, "min_call_ms": min(t) * 1e3,
+            "setting": "glibc arena reuse (mallopt M_MMAP_MAX=0, M_TRIM_THRESHOLD=2^31-1), all host threads"}
+
+
 def cpu_rows(kernel, dtype, domain, cores, seconds=4.0):
-    """SURVEY.md 8(d) secondary CPU rows: the gen kernel on 1 thread, and the
-    reference's NumPy engine (vec) through its own compile_stencil."""
+    """SURVEY.md 8(d) secondary CPU rows: the gen kernel on 1 thread, the gen
+    kernel with glibc arena reuse, and the reference's NumPy engine (vec)
+    through its own compile_stencil."""
     rows = {}
     pts = domain[0] * domain[1] * domain[2]
+    ar = arena_reuse_row(kernel, dtype, domain, seconds=seconds)
+    if ar is not None:
+        rows["gen_arena_reuse"] = ar
     os.environ["GTS_NUM_THREADS"] = "1"  # read by the generated C on every call (gen.py:296-299)
     try:
         t1 = time_reference(kernel, dtype, domain, seconds=seconds, max_calls=50, warmup=1)
@@ -301,6 +332,9 @@ def run_reference(args, dist):
                                    f"OpenMP over all {cores} host threads ({model})"},
         "e2e": {"value": value, "unit": "grid-points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    ar = arena_reuse_row(kernel, dtype, domain, seconds=8.0)
+    if ar is not None:
+        line["cpu_baseline"]["rows"] = {"gen_arena_reuse": ar}
     print(json.dumps(line))
 
 
