@@ -568,6 +568,48 @@ def dycore_decomposed_peer(dist, steps=20, tile=(512, 512, 80)):
             "value": pts / (ms / 1e3), "unit": "grid-point-steps/s", "ms_per_step": ms, "scaling": "weak"}
 
 
+def dycore_fused_peer(dist, steps=20, tile=(512, 512, 80)):
+    """The dycore step with the halo exchange fused into the producing kernel
+    (decomp.PeerFusedStep: the column kernel's epilogue also stores the
+    boundary of u_out into the neighbours' halos over peer memory, one launch
+    + a flag wait and signal per step), a 512x512x80 tile per GPU, ``steps``
+    steps replayed from one CUDA graph; max over ranks.  At N=1 there are no
+    neighbours: the same kernel with an empty mirror."""
+    import paper_2311_08322_b200 as b200
+    from paper_2311_08322_b200 import decomp, native, workloads
+
+    grid = decomp.choose_grid(dist.world)
+    gdom = (tile[0] * grid[0], tile[1] * grid[1], tile[2])
+    d = decomp.Decomposition(gdom, grid, dist.rank)
+    arr = workloads.dycore_arrays(d.local_domain, 2000 + dist.rank)
+    st = b200.compile_stencil(workloads.source("dycore"), "dycore", gen_options={"mirror": "u_out"})
+    A, B = b200.from_array(arr["u"], (2, 2, 0)), b200.from_array(arr["u"], (2, 2, 0))
+    coef = {n: b200.from_array(arr[n]) for n in "abc"}
+    step = decomp.PeerFusedStep(st, d, [{"u_in": A, "u_out": B, **coef}, {"u_in": B, "u_out": A, **coef}],
+                                workloads.DYCORE_SCALARS, "u_out", (2, 2))
+    for _ in range(4):
+        step()
+    native.synchronize(step.stream)
+    g = step.graph(steps)
+    g.launch()
+    native.synchronize(step.stream)
+    e0, e1 = native.Event(), native.Event()
+    dist.barrier()
+    e0.record(step.stream)
+    g.launch()
+    e1.record(step.stream)
+    native.synchronize(step.stream)
+    dist.barrier()
+    ms = dist.max(e0.elapsed_ms(e1) / steps)
+    step.close()
+    pts = gdom[0] * gdom[1] * gdom[2]
+    return {"workload": f"dycore step, {tile[0]}x{tile[1]}x{tile[2]} per GPU on a {grid[0]}x{grid[1]} grid "
+                        f"(global {gdom[0]}x{gdom[1]}x{gdom[2]}), u_out boundary stored into the neighbours' "
+                        f"halos by the column kernel itself, {steps} steps replayed from one CUDA graph",
+            "value": pts / (ms / 1e3), "unit": "grid-point-steps/s", "ms_per_step": ms, "scaling": "weak",
+            "launches_per_step": 3 if dist.world > 1 else 1}
+
+
 def dycore_timed(dist, steps=100, domain=(512, 512, 80), reps=3, gen_options=None):
     """BASELINE.json configs[4]: the dycore-like step (kernels/dycore.gts:
     hdiff -> Thomas solve -> interval-specialised update) on 512x512x80 f64,
@@ -720,9 +762,15 @@ def run_b200(args, dist):
             dy_peer = dycore_decomposed_peer(dist)
         except Exception as exc:  # pragma: no cover - reported, not fatal
             dy_peer = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+    dy_fused = None
+    if not args.no_extra and dist.world > 1:
+        try:
+            dy_fused = dycore_fused_peer(dist)
+        except Exception as exc:  # pragma: no cover - reported, not fatal
+            dy_fused = {"error": f"{type(exc).__name__}: {exc}"[:300]}
     if dist.rank == 0 and dist.world > 1:
         line["extra"] = {"hdiff_decomposed": decomp_line, "hdiff_decomposed_peer": peer_line,
-                         "dycore_decomposed_peer": dy_peer}
+                         "dycore_decomposed_peer": dy_peer, "dycore_fused_peer": dy_fused}
     if dist.rank == 0 and dist.world == 1 and not args.no_extra:
         extra = {}
         for name in ("hdiff", "hdiff32"):
@@ -771,6 +819,10 @@ def run_b200(args, dist):
             extra["dycore"] = dy
         except Exception as exc:  # pragma: no cover - reported, not fatal
             extra["dycore"] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+        try:
+            extra["dycore_fused_peer"] = dycore_fused_peer(dist)
+        except Exception as exc:  # pragma: no cover - reported, not fatal
+            extra["dycore_fused_peer"] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
         line["extra"] = extra
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
         cores, model = host_info()

@@ -147,6 +147,13 @@ int gts_b200_ipc_close(void* dptr);
 int gts_b200_copy_box(void* dst, int64_t d_i, int64_t d_j, int64_t d_k, const void* src,
                       int64_t s_i, int64_t s_j, int64_t s_k, int64_t ni, int64_t nj, int64_t nk,
                       int itemsize, void* stream);
+/* n (<= 8) flags at once: add 1 to each (system-scope release, after a
+ * system fence), and wait until each reaches its next expected count (one
+ * device-resident u64 per flag).  decomp.PeerFusedStep: one launch per step
+ * for all neighbours. */
+int gts_b200_flags_add(void* const* flags, int n, void* stream);
+int gts_b200_flags_wait_next(void* const* flags, void* expected, int n, void* stream);
+
 int gts_b200_flag_signal(void* flag, uint64_t value, void* stream);
 /* Graph-capturable forms: flag_add adds 1 (system-scope release);
  * flag_wait_next bumps the consumer's own expected count (a 64-bit word in

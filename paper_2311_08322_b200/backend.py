@@ -25,7 +25,7 @@ from typing import Optional
 
 from . import native
 from ._host import BackendError, Code, ir, sf_common
-from .codegen import entry_name, generate_source
+from .codegen import entry_name, generate_source, mirror_setter_name
 from .lowering import build_plan
 from .storage import DeviceFieldStorage, FieldStorage
 from .toolchain import BuildCache, load_library
@@ -96,6 +96,23 @@ class Module:
         self.field_order = [f.name for f in impl.api_fields]
         self.scalar_order = [s.name for s in impl.api_scalars]
         self.written = sf_common.written_fields(impl)
+        try:  # present when built with gen_options mirror
+            self._mirror_fn = getattr(self.lib, mirror_setter_name(impl, fp))
+            self._mirror_fn.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_int64)]
+            self._mirror_fn.restype = ctypes.c_int
+        except AttributeError:
+            self._mirror_fn = None
+
+    def set_mirror(self, boxes) -> None:
+        """Halo-mirror boxes for the next launches (gen_options ``mirror``):
+        ``boxes`` = [(i0, i1, j0, j1, base_address, s_i, s_j, s_k)], at most 8,
+        in the launch's domain coordinates; element (i, j, k) of a box is also
+        stored at base + (i*s_i + j*s_j + k*s_k) * itemsize."""
+        if self._mirror_fn is None:
+            raise BackendError(Code.COMPILE_FAILED, "module was not built with gen_options mirror")
+        flat = [int(x) for b in boxes for x in b]
+        arr = (ctypes.c_int64 * max(1, len(flat)))(*flat)
+        native.check(self._mirror_fn(len(boxes), arr), "set mirror")
 
     def bind_device(self) -> None:
         dev = native.current_device()

@@ -471,6 +471,28 @@ def generate_source(plan: Plan, fp, options: Optional[dict] = None) -> str:
         return _generate_source(plan, fp, options)
 
 
+def mirror_setter_name(impl, fp) -> str:
+    """Exported setter of the halo-mirror boxes (gen_options ``mirror``)."""
+    return "gts_mirror_" + entry_name(impl, fp)[len("gts_run_"):]
+
+
+def _mirror_field(plan: Plan, opts: dict):
+    """gen_options ``mirror``: the api output field whose stores the column
+    template also sends into neighbour halos (decomp.PeerFusedStep).  Only
+    a field written by exactly one column kernel (the TMEM template, whose
+    launch refuses to fall back) can be mirrored."""
+    m = opts.get("mirror")
+    if not m:
+        return None
+    if m not in {f.name for f in plan.impl.api_fields}:
+        raise ValueError(f"gen_options mirror: '{m}' is not an api field")
+    writers = [k for k in plan.kernels if any(m in writes(r.stage.body) for r in k.stages)]
+    if len(writers) != 1 or writers[0].kind != "column":
+        raise ValueError(f"gen_options mirror: '{m}' must be written by exactly one column kernel "
+                         f"(plan {' '.join(plan.describe())})")
+    return m
+
+
 def _generate_source(plan: Plan, fp, options: Optional[dict] = None) -> str:
     impl = plan.impl
     from . import codegen_column, codegen_parallel, codegen_rowstream  # template instantiations
@@ -500,6 +522,7 @@ def _generate_source(plan: Plan, fp, options: Optional[dict] = None) -> str:
             for t in k.local_temps:
                 local_of[t] = kidx
     arena_temps = list(plan.global_temps) + sorted(local_of)
+    mirror = _mirror_field(plan, opts)
     w("struct GtsParams {")
     w("  int ni, nj, nk;")
     for f in impl.api_fields:
@@ -509,8 +532,28 @@ def _generate_source(plan: Plan, fp, options: Optional[dict] = None) -> str:
         w(f"  GtsField<{ctype[t]}> f_{t};")
     for s in impl.api_scalars:
         w(f"  double sc_{s.name};")
+    if mirror:
+        w(f"  GtsMirror<{ctype[mirror]}> mir;")
     w("};")
     w("")
+    if mirror:
+        # host-side mirror boxes, set by gts_mirror_<name>_<digest8> and copied
+        # into every launch's parameters (so a CUDA graph captures the boxes
+        # that were set when the launch was captured)
+        w(f"static GtsMirror<{ctype[mirror]}> g_mirror;")
+        w('extern "C" __attribute__((visibility("default")))')
+        w(f"int {mirror_setter_name(impl, fp)}(int n, const int64_t* desc) {{")
+        w(f"  if (n < 0 || n > 8) return {GTS_ERR_UNSUPPORTED};")
+        w("  g_mirror.n = n;")
+        w("  for (int d = 0; d < n; ++d) {")
+        w("    const int64_t* q = desc + 8 * d;")
+        w("    g_mirror.i0[d] = (int)q[0]; g_mirror.i1[d] = (int)q[1]; g_mirror.j0[d] = (int)q[2]; g_mirror.j1[d] = (int)q[3];")
+        w(f"    g_mirror.base[d] = ({ctype[mirror]}*)(intptr_t)q[4];")
+        w("    g_mirror.si[d] = q[5]; g_mirror.sj[d] = q[6]; g_mirror.sk[d] = q[7];")
+        w("  }")
+        w("  return 0;")
+        w("}")
+        w("")
 
     launches: list = []  # host-side launch code lines
     prelude: list = []  # host-side lines before the arena is sized
@@ -677,6 +720,8 @@ def _generate_source(plan: Plan, fp, options: Optional[dict] = None) -> str:
         elif k.kind == "column":
             out.extend(_column_kernel(kname, plan, k, ctype, dtypes))
             sp = codegen_column.spec(plan, k, dtypes) if opts.get("tmem", True) else None
+            if sp is None and mirror and any(mirror in writes(r.stage.body) for r in k.stages):
+                raise ValueError(f"gen_options mirror: '{mirror}' needs the TMEM column template")
             if sp is not None:
                 code, launch = codegen_column.emit(kname, plan, k, sp, ctype, dtypes, opts)
                 out.extend(code)
@@ -716,6 +761,8 @@ def _generate_source(plan: Plan, fp, options: Optional[dict] = None) -> str:
         w(f"  p.f_{n} = gts_field(f_{n}, s_{n}_i, s_{n}_j, s_{n}_k, o_{n}_i, o_{n}_j, o_{n}_k);")
     for s in impl.api_scalars:
         w(f"  p.sc_{s.name} = sc_{s.name};")
+    if mirror:
+        w("  p.mir = g_mirror;")
     out.extend(prelude)
     if arena_temps:
         w("  // device arena for temporaries: shape = domain + extent (common.py:58-69),")

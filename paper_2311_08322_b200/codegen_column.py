@@ -33,7 +33,7 @@ from dataclasses import dataclass, field
 from typing import Optional
 
 from ._host import ir
-from .codegen import DivPool, _bound, _interval_groups, _MemCtx, c_float, emit_cond, emit_expr  # noqa: F401
+from .codegen import GTS_ERR_UNSUPPORTED, DivPool, _bound, _interval_groups, _MemCtx, c_float, emit_cond, emit_expr  # noqa: F401
 from . import codegen_prologue
 from .lowering import always_writes, reads, writes
 
@@ -250,6 +250,7 @@ class _Ctx(_MemCtx):
 
 
 _NOSTORE = False
+_MIRROR = None  # gen_options mirror: api field whose stores also go to neighbour halos
 
 
 def _emit_stmt(stmt, ctx: _Ctx, ctype, api: set, indent: str, out: list) -> None:
@@ -441,6 +442,8 @@ def emit(kname: str, plan, kplan, sp: ThomasSpec, ctype: dict, dtypes: dict, opt
         launch.append("        launched = true;")
         launch.append("      }")
         launch.append("    }")
+    if (opts or {}).get("mirror"):
+        fallback = [f"  return {GTS_ERR_UNSUPPORTED};  // a mirrored field needs this template"]
     if fallback is None:
         fallback = [
             "  {",
@@ -463,8 +466,9 @@ def _emit_variant(kname, plan, sp: ThomasSpec, v: Variant, ctype, dtypes, opts):
     generic per-level-checked body covers partial stages and group
     boundaries."""
     dbg = (opts or {}).get("tmem_debug", "")
-    global _NOSTORE
+    global _NOSTORE, _MIRROR
     _NOSTORE = dbg == "nostore"
+    _MIRROR = (opts or {}).get("mirror") or None
     impl = plan.impl
     api = {f.name for f in impl.api_fields}
     msf, msb = impl.multistages[sp.ms_f], impl.multistages[sp.ms_b]
@@ -939,6 +943,46 @@ def _emit_variant(kname, plan, sp: ThomasSpec, v: Variant, ctype, dtypes, opts):
         epilogue_level("        ", lambda f: "GTS_NAN")
         w("      }")
     if dbg in ("fwdonly", "streamonly"):
+        w("      }")
+    if _MIRROR:
+        # gen_options mirror: the tile's columns that lie in a neighbour's halo
+        # (up to 3: i-face, j-face, corner) send their finished column of the
+        # mirrored field there (peer stores), re-read from this thread's own
+        # stores; kept out of the level loops so they keep their registers
+        t_ = ctype[_MIRROR]
+        w("      {")
+        w(f"        {t_}* mp0_ = nullptr; {t_}* mp1_ = nullptr; {t_}* mp2_ = nullptr;")
+        w("        long long mk0_ = 0, mk1_ = 0, mk2_ = 0;")
+        w("        int nm_ = 0;")
+        w("        if (valid) {")
+        w("          for (int d = 0; d < p.mir.n; ++d) {")
+        w("            if (i < p.mir.i0[d] || i >= p.mir.i1[d] || j < p.mir.j0[d] || j >= p.mir.j1[d]) continue;")
+        w(f"            {t_}* const q_ = p.mir.base[d] + (long long)i * p.mir.si[d] + (long long)j * p.mir.sj[d];")
+        w("            if (nm_ == 0) { mp0_ = q_; mk0_ = p.mir.sk[d]; }")
+        w("            else if (nm_ == 1) { mp1_ = q_; mk1_ = p.mir.sk[d]; }")
+        w("            else { mp2_ = q_; mk2_ = p.mir.sk[d]; }")
+        w("            ++nm_;")
+        w("          }")
+        w("        }")
+        w("        if (nm_ > 0) {")
+        w(f"          const {t_}* const src_ = colp_{_MIRROR};")
+        w(f"          const long long sk_ = p.f_{_MIRROR}.sk;")
+        MB = int((opts or {}).get("mirror_batch", 16))
+        w(f"          // {MB} levels in flight per batch: all loads, then all stores")
+        w(f"          for (int kb = 0; kb < nk; kb += {MB}) {{")
+        w(f"            {t_} v_[{MB}];")
+        w("            #pragma unroll")
+        w(f"            for (int u = 0; u < {MB}; ++u) if (kb + u < nk) v_[u] = src_[(long long)(kb + u) * sk_];")
+        w("            #pragma unroll")
+        w(f"            for (int u = 0; u < {MB}; ++u) {{")
+        w("              if (kb + u >= nk) break;")
+        w("              const long long k = kb + u;")
+        w("              mp0_[k * mk0_] = v_[u];")
+        w("              if (mp1_) mp1_[k * mk1_] = v_[u];")
+        w("              if (mp2_) mp2_[k * mk2_] = v_[u];")
+        w("            }")
+        w("          }")
+        w("        }")
         w("      }")
     w("      __syncwarp();")
     w("    }")

@@ -375,6 +375,56 @@ GTS_EXPORT int gts_b200_flag_wait_next(const void* flag, void* expected, void* s
   return (int)cudaGetLastError();
 }
 
+// n flags at once (up to 8; decomp.PeerFusedStep signals and waits for all
+// its neighbours with one launch each instead of one per neighbour)
+struct GtsFlagSet {
+  unsigned long long* p[8];
+};
+
+__global__ void gts_flags_add_kernel(GtsFlagSet f, int n) {
+  const int d = threadIdx.x;
+  if (d >= n) return;
+  __threadfence_system();  // the previous kernels' peer stores before the release
+  asm volatile("red.release.sys.global.add.u64 [%0], 1;" ::"l"(f.p[d]) : "memory");
+}
+
+__global__ void gts_flags_wait_next_kernel(GtsFlagSet f, unsigned long long* expected, int n) {
+  const int d = threadIdx.x;
+  if (d < n) {
+    const unsigned long long e = expected[d] + 1ull;
+    expected[d] = e;
+    unsigned long long v;
+    for (;;) {
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(f.p[d]) : "memory");
+      if ((long long)(v - e) >= 0) break;
+      __nanosleep(256);
+    }
+  }
+  __syncthreads();
+}
+
+static int gts_flag_set(GtsFlagSet* f, void* const* flags, int n) {
+  if (n < 0 || n > 8) return (int)cudaErrorInvalidValue;
+  for (int d = 0; d < 8; ++d) f->p[d] = d < n ? (unsigned long long*)flags[d] : nullptr;
+  return 0;
+}
+
+GTS_EXPORT int gts_b200_flags_add(void* const* flags, int n, void* stream) {
+  GtsFlagSet f;
+  if (int e = gts_flag_set(&f, flags, n)) return e;
+  if (n == 0) return 0;
+  gts_flags_add_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(f, n);
+  return (int)cudaGetLastError();
+}
+
+GTS_EXPORT int gts_b200_flags_wait_next(void* const* flags, void* expected, int n, void* stream) {
+  GtsFlagSet f;
+  if (int e = gts_flag_set(&f, flags, n)) return e;
+  if (n == 0) return 0;
+  gts_flags_wait_next_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(f, (unsigned long long*)expected, n);
+  return (int)cudaGetLastError();
+}
+
 GTS_EXPORT int gts_b200_flag_signal(void* flag, uint64_t value, void* stream) {
   gts_flag_signal_kernel<<<1, 1, 0, (cudaStream_t)stream>>>((unsigned long long*)flag,
                                                             (unsigned long long)value);

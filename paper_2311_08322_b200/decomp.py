@@ -531,3 +531,174 @@ class PeerDecomposedStep:
         if self.exchanger.peer:
             self.exchanger.acknowledge(self.compute)
             self.exchanger.field.mark_device_written()  # neighbours rewrote its halo
+
+
+DIRS8 = [(-1, -1), (-1, 0), (-1, 1), (0, -1), (0, 1), (1, -1), (1, 0), (1, 1)]
+
+
+def mirror_boxes(decomp: Decomposition, halo: tuple) -> list:
+    """For each existing neighbour in DIRS8 order: (direction index, rank, box)
+    with box = (i0, i1, j0, j1), the cells of our local domain that lie in
+    that neighbour's halo (faces: the ``halo``-deep boundary band over the
+    full other extent; corners: the halo x halo corner)."""
+    ni, nj, _ = decomp.local_domain
+    hi, hj = halo
+    out = []
+    for d, (di, dj) in enumerate(DIRS8):
+        nb = decomp.neighbour(di, dj)
+        if nb is None:
+            continue
+        i0, i1 = {-1: (0, hi), 0: (0, ni), 1: (ni - hi, ni)}[di]
+        j0, j1 = {-1: (0, hj), 0: (0, nj), 1: (nj - hj, nj)}[dj]
+        out.append((d, nb, (max(i0, 0), min(i1, ni), max(j0, 0), min(j1, nj))))
+    return out
+
+
+class PeerFusedStep:
+    """One decomposed time step in ONE kernel launch: the producing kernel
+    itself stores the boundary values of its output into the neighbours'
+    halos (peer memory: NVLink / NVSwitch between GPUs, CUDA IPC within one),
+    so there is no separate exchange, pack or copy -- the transfer overlaps
+    the computation tile by tile (the dycore step, one halo
+    exchange per step, fused into the producer).
+
+    ``phases``: field bindings cycled step by step (the dycore's u_in / u_out
+    swap: ``[{u_in: A, u_out: B, ...}, {u_in: B, u_out: A, ...}]``); the
+    stencil is compiled with ``gen_options={"mirror": out_field}`` so its
+    column kernel stores ``out_field`` also through the mirror boxes
+    (``Module.set_mirror``: up to 8 neighbours, corners included, each cell
+    sent by its owner).  Per step, on one stream: wait until every neighbour
+    finished its previous step (``gts_b200_flags_wait_next``: its stores into
+    our input's halo are complete, and it no longer reads the halo of the
+    buffer we are about to write into), launch, then bump every neighbour's
+    counter (``gts_b200_flags_add``).  The result is bitwise the undecomposed
+    run's (the same instructions per point; halos arrive before they are
+    read)."""
+
+    def __init__(self, stencil, decomposition: Decomposition, phases: list, scalars: dict,
+                 out_field: str, halo: tuple, group=None, stream: Optional[int] = None):
+        import ctypes
+
+        import torch.distributed as dist
+
+        from . import native, storage
+
+        module = stencil.build_info["module"]
+        if getattr(module, "_mirror_fn", None) is None:
+            raise ValueError(f"compile the stencil with gen_options={{'mirror': '{out_field}'}}")
+        self.native, self.module, self.decomp = native, module, decomposition
+        self.stream = native.default_stream() if stream is None else stream
+        self.phases = phases
+        self.out_field = out_field
+        dom = decomposition.local_domain
+        self._flags = storage._DeviceBuffer(64, pinned_host=False)  # ARRIVED[8], one per direction
+        self._expect = storage._DeviceBuffer(64, pinned_host=False)
+        native.call("gts_b200_memset", self._flags.dptr, 0, 64, self.stream)
+        native.call("gts_b200_memset", self._expect.dptr, 0, 64, self.stream)
+        native.synchronize(self.stream)
+
+        outs = []  # distinct output storages across phases, shared with the neighbours
+        for ph in phases:
+            f = ph[out_field]
+            if not isinstance(f, storage.DeviceFieldStorage):
+                raise TypeError("PeerFusedStep needs DeviceFieldStorages")
+            if all(f is not o for o in outs):
+                outs.append(f)
+
+        def handle(ptr):
+            h, off = ctypes.create_string_buffer(64), ctypes.c_size_t()
+            native.call("gts_b200_ipc_get_handle", ptr, h, ctypes.byref(off))
+            return h.raw, off.value
+
+        self._opened = []
+        self.neighbours = mirror_boxes(decomposition, halo)
+        single = tuple(decomposition.grid) == (1, 1)  # no neighbours, no process group needed
+        allv = []
+        if not single:
+            me = {"outs": [(handle(f.base_address()), tuple(f.strides), tuple(f.origin)) for f in outs],
+                  "flags": handle(self._flags.dptr), "box": (decomposition.i0, decomposition.j0)}
+            allv = [None] * dist.get_world_size(group)
+            dist.all_gather_object(allv, me, group=group)
+        remote_outs, self._remote_flags, self._my_flags = {}, [], []
+        for d, nb, box in self.neighbours:
+            info = allv[nb]
+            gp = ctypes.c_void_p()
+            native.call("gts_b200_ipc_open", info["flags"][0], ctypes.byref(gp))
+            self._opened.append(gp.value)
+            opp = DIRS8.index(tuple(-x for x in DIRS8[d]))
+            self._remote_flags.append(gp.value + info["flags"][1] + 8 * opp)
+            self._my_flags.append(self._flags.dptr + 8 * d)
+            for oi, ((h, off), strides, origin) in enumerate(info["outs"]):
+                fp = ctypes.c_void_p()
+                native.call("gts_b200_ipc_open", h, ctypes.byref(fp))
+                self._opened.append(fp.value)
+                remote_outs[(d, oi)] = (fp.value + off, strides, origin, info["box"])
+        n = len(self.neighbours)
+        self._n = n
+        self._remote_arr = (ctypes.c_void_p * max(1, n))(*self._remote_flags)
+        self._my_arr = (ctypes.c_void_p * max(1, n))(*self._my_flags)
+        # per phase: the mirror boxes into the neighbours' copy of that phase's output
+        self._boxes, self._launch = [], []
+        item = outs[0].itemsize
+        I0, J0 = decomposition.i0, decomposition.j0
+        for ph in phases:
+            oi = next(x for x, f in enumerate(outs) if f is ph[out_field])
+            boxes = []
+            for d, nb, (bi0, bi1, bj0, bj1) in self.neighbours:
+                base, (si, sj, sk), (oi_, oj_, ok_), (nI0, nJ0) = remote_outs[(d, oi)]
+                # our local (i, j) -> neighbour storage element origin + (I0 - nI0 + i, J0 - nJ0 + j)
+                off = (oi_ + I0 - nI0) * si + (oj_ + J0 - nJ0) * sj + ok_ * sk
+                boxes.append((bi0, bi1, bj0, bj1, base + off * item, si, sj, sk))
+            self._boxes.append(boxes)
+            self._launch.append(module.launcher(dom, ph, scalars, self.stream))
+        self._step = 0
+        if not single:
+            dist.barrier(group)  # every rank mapped its peers
+            # the initial halos are valid and no buffer is being read: one
+            # arrival per neighbour lets everyone's first step start
+            native.call("gts_b200_flags_add", self._remote_arr, n, self.stream)
+            native.synchronize(self.stream)
+            dist.barrier(group)
+
+    def __call__(self) -> None:
+        p = self._step % len(self.phases)
+        self.native.call("gts_b200_flags_wait_next", self._my_arr, self._expect.dptr, self._n, self.stream)
+        self.module.set_mirror(self._boxes[p])
+        self._launch[p]()
+        self.native.call("gts_b200_flags_add", self._remote_arr, self._n, self.stream)
+        self._step += 1
+
+    def graph(self, steps: int):
+        """``steps`` steps (a multiple of the phase count, so every replay
+        starts at the same phase) captured into one CUDA graph."""
+        if steps % len(self.phases) or self._step % len(self.phases):
+            raise ValueError(f"capture at phase 0, a multiple of {len(self.phases)} steps")
+        g = self.native.Graph(self.stream)
+        start = self._step
+        with g.capture():
+            for _ in range(steps):
+                self()
+        self._step = start
+        outs = [ph[self.out_field] for ph in self.phases]
+        outer = self
+
+        class _Replay:
+            graph = g
+
+            def launch(self_) -> None:
+                if outer._step % len(outer.phases):
+                    raise RuntimeError("replay must start at phase 0")
+                g.launch()
+                outer._step += steps
+                for f in outs:  # written here and by the neighbours: host mirrors are stale
+                    f.mark_device_written()
+
+        return _Replay()
+
+    def close(self) -> None:
+        for p in self._opened:
+            try:
+                self.native.call("gts_b200_ipc_close", p)
+            except Exception:  # pragma: no cover - teardown
+                pass
+        self._opened = []

@@ -48,6 +48,8 @@ SIGNATURES = {
     "gts_b200_event_record": (_INT, [_VP, _VP]),
     "gts_b200_event_synchronize": (_INT, [_VP]),
     "gts_b200_event_record_dep": (_INT, [_VP, _VP]),
+    "gts_b200_flags_add": (_INT, [_VP, _INT, _VP]),
+    "gts_b200_flags_wait_next": (_INT, [_VP, _VP, _INT, _VP]),
     "gts_b200_event_elapsed_ms": (_INT, [_c.POINTER(_c.c_float), _VP, _VP]),
     "gts_b200_l2_flush": (_INT, [_VP]),
     "gts_b200_pack_box": (_INT, [_VP, _VP] + [_I64] * 9 + [_INT, _VP]),

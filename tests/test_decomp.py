@@ -223,3 +223,58 @@ def test_peer_dycore_decomposed_multiprocess():
            str(repo / "tools" / "peer_dycore_check.py"), "4"]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=str(repo))
     assert r.returncode == 0 and r.stdout.count("DYCORE_PEER_OK") == 2, (r.stdout[-2000:], r.stderr[-3000:])
+
+
+@pytest.mark.parametrize("grid", [(2, 1), (1, 2), (2, 2), (4, 2), (3, 3)])
+def test_mirror_boxes_cover_every_halo_once(grid):
+    """decomp.mirror_boxes (PeerFusedStep): the cells every rank sends into
+    its neighbours' halos are exactly those neighbours' 2-deep halo cells
+    inside the global domain (faces and corners), each sent once, by its
+    owner."""
+    from paper_2311_08322_b200 import decomp
+
+    gdom = (9 * grid[0] + 3, 11 * grid[1] + 5, 4)
+    h = (2, 2)
+    ranks = [decomp.Decomposition(gdom, grid, r) for r in range(grid[0] * grid[1])]
+    got = {r: [] for r in range(len(ranks))}
+    for d in ranks:
+        for di, nb, (i0, i1, j0, j1) in decomp.mirror_boxes(d, h):
+            for i in range(i0, i1):
+                for j in range(j0, j1):
+                    got[nb].append((d.i0 + i, d.j0 + j))
+    for n in ranks:
+        want = sorted((gi, gj)
+                      for gi in range(max(0, n.i0 - h[0]), min(gdom[0], n.i1 + h[0]))
+                      for gj in range(max(0, n.j0 - h[1]), min(gdom[1], n.j1 + h[1]))
+                      if not (n.i0 <= gi < n.i1 and n.j0 <= gj < n.j1))
+        assert sorted(got[n.rank]) == want, n.rank
+
+
+def test_mirror_option_rejects_unsupported_fields():
+    """gen_options mirror needs an api field written by one column kernel."""
+    import paper_2311_08322_b200 as b200
+    from paper_2311_08322_b200 import workloads
+
+    for src, name, field in ((workloads.source("hdiff"), "hdiff", "out"),
+                             (workloads.source("dycore"), "dycore", "lap")):
+        with pytest.raises(Exception, match="mirror"):
+            b200.compile_stencil(src, name, gen_options={"mirror": field})
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("nproc,steps", [(2, 4), (4, 2)])
+def test_peer_fused_dycore_multiprocess(nproc, steps):
+    """The dycore step with the halo exchange fused into the producing
+    kernel (PeerFusedStep, peer stores from the column kernel's epilogue,
+    corners included): bitwise the undecomposed oracle, eager and replayed
+    from a CUDA graph, with 2 and 4 processes sharing one B200."""
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    repo = Path(__file__).resolve().parent.parent
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           str(repo / "tools" / "peer_fused_check.py"), str(steps)]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=400, cwd=str(repo))
+    assert r.returncode == 0 and r.stdout.count("FUSED_PEER_OK") == nproc, (r.stdout[-2000:], r.stderr[-3000:])

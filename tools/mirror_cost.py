@@ -1,0 +1,56 @@
+"""Cost of the fused halo stores of decomp.PeerFusedStep on one GPU: the
+dycore step (512x512x80 per GPU) with an empty mirror, and with the 8 mirror
+boxes an interior rank of a 3x3 grid has (2-deep faces and corners), here
+pointed at a scratch field on the same GPU instead of the neighbours' halos
+(so the extra pass writes local HBM instead of NVLink).  CUDA-graph timed,
+20 steps per replay, median of 5 replays."""
+import statistics
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import paper_2311_08322_b200 as b200  # noqa: E402
+from paper_2311_08322_b200 import decomp, native, workloads  # noqa: E402
+
+dom = (512, 512, 80)
+d = decomp.Decomposition(dom, (1, 1), 0)
+arr = workloads.dycore_arrays(dom, 7)
+opts = {"mirror": "u_out"}
+if len(sys.argv) > 1:
+    opts["mirror_batch"] = int(sys.argv[1])
+st = b200.compile_stencil(workloads.source("dycore"), "dycore", gen_options=opts)
+A, B = b200.from_array(arr["u"], (2, 2, 0)), b200.from_array(arr["u"], (2, 2, 0))
+S = b200.from_array(arr["u"], (2, 2, 0))  # scratch "neighbour halo"
+coef = {n: b200.from_array(arr[n]) for n in "abc"}
+step = decomp.PeerFusedStep(st, d, [{"u_in": A, "u_out": B, **coef}, {"u_in": B, "u_out": A, **coef}],
+                            workloads.DYCORE_SCALARS, "u_out", (2, 2))
+ni, nj, _ = dom
+fake = []
+for di in (-1, 0, 1):
+    for dj in (-1, 0, 1):
+        if di == dj == 0:
+            continue
+        i0, i1 = {-1: (0, 2), 0: (0, ni), 1: (ni - 2, ni)}[di]
+        j0, j1 = {-1: (0, 2), 0: (0, nj), 1: (nj - 2, nj)}[dj]
+        org = sum(o * s for o, s in zip(S.origin, S.strides)) * S.itemsize
+        fake.append((i0, i1, j0, j1, S.base_address() + org, *S.strides))
+
+
+def timed(boxes):
+    step._boxes = [boxes, boxes]
+    g = step.graph(20)
+    g.launch()
+    native.synchronize(step.stream)
+    out = []
+    for _ in range(5):
+        e0, e1 = native.Event(), native.Event()
+        e0.record(step.stream)
+        g.launch()
+        e1.record(step.stream)
+        native.synchronize(step.stream)
+        out.append(e0.elapsed_ms(e1) / 20 * 1e3)
+    return statistics.median(out)
+
+
+for label, boxes in (("no neighbours", []), ("8 neighbours (3x3 interior rank)", fake), ("no neighbours", [])):
+    print(f"dycore 512x512x80 fused-halo step {opts}, {label}: {timed(boxes):.2f} us/step", flush=True)
