@@ -16,7 +16,7 @@ dom = (512, 512, 80)
 d = decomp.Decomposition(dom, (1, 1), 0)
 arr = workloads.dycore_arrays(dom, 7)
 opts = {"mirror": "u_out"}
-if len(sys.argv) > 1:
+if len(sys.argv) > 1 and sys.argv[1].isdigit():
     opts["mirror_batch"] = int(sys.argv[1])
 st = b200.compile_stencil(workloads.source("dycore"), "dycore", gen_options=opts)
 A, B = b200.from_array(arr["u"], (2, 2, 0)), b200.from_array(arr["u"], (2, 2, 0))
@@ -52,5 +52,10 @@ def timed(boxes):
     return statistics.median(out)
 
 
-for label, boxes in (("no neighbours", []), ("8 neighbours (3x3 interior rank)", fake), ("no neighbours", [])):
+sel = {"i-faces only": [fake[1], fake[6]], "j-faces only": [fake[3], fake[4]],
+       "corners only": [fake[0], fake[2], fake[5], fake[7]]}
+runs = [("no neighbours", []), ("8 neighbours (3x3 interior rank)", fake), ("no neighbours", [])]
+if "--split" in sys.argv:
+    runs += list(sel.items())
+for label, boxes in runs:
     print(f"dycore 512x512x80 fused-halo step {opts}, {label}: {timed(boxes):.2f} us/step", flush=True)
