@@ -965,21 +965,20 @@ def _emit_variant(kname, plan, sp: ThomasSpec, v: Variant, ctype, dtypes, opts):
         w("          }")
         w("        }")
         w("        if (nm_ > 0) {")
-        w(f"          const {t_}* const src_ = colp_{_MIRROR};")
+        w(f"          const {t_}* src_ = colp_{_MIRROR};")
         w(f"          const long long sk_ = p.f_{_MIRROR}.sk;")
         MB = int((opts or {}).get("mirror_batch", 16))
-        w(f"          // {MB} levels in flight per batch: all loads, then all stores")
+        w(f"          // {MB} levels in flight per batch (all loads, then all stores), running pointers")
         w(f"          for (int kb = 0; kb < nk; kb += {MB}) {{")
         w(f"            {t_} v_[{MB}];")
         w("            #pragma unroll")
-        w(f"            for (int u = 0; u < {MB}; ++u) if (kb + u < nk) v_[u] = src_[(long long)(kb + u) * sk_];")
+        w(f"            for (int u = 0; u < {MB}; ++u) {{ if (kb + u < nk) v_[u] = *src_; src_ += sk_; }}")
         w("            #pragma unroll")
         w(f"            for (int u = 0; u < {MB}; ++u) {{")
         w("              if (kb + u >= nk) break;")
-        w("              const long long k = kb + u;")
-        w("              mp0_[k * mk0_] = v_[u];")
-        w("              if (mp1_) mp1_[k * mk1_] = v_[u];")
-        w("              if (mp2_) mp2_[k * mk2_] = v_[u];")
+        w("              *mp0_ = v_[u]; mp0_ += mk0_;")
+        w("              if (mp1_) { *mp1_ = v_[u]; mp1_ += mk1_; }")
+        w("              if (mp2_) { *mp2_ = v_[u]; mp2_ += mk2_; }")
         w("            }")
         w("          }")
         w("        }")

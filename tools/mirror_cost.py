@@ -52,6 +52,12 @@ def timed(boxes):
     return statistics.median(out)
 
 
+if "--eager" in sys.argv:  # profiler runs: a few plain steps with the 8 boxes, no graph
+    step._boxes = [fake, fake]
+    for _ in range(4):
+        step()
+    native.synchronize(step.stream)
+    sys.exit(0)
 sel = {"i-faces only": [fake[1], fake[6]], "j-faces only": [fake[3], fake[4]],
        "corners only": [fake[0], fake[2], fake[5], fake[7]]}
 runs = [("no neighbours", []), ("8 neighbours (3x3 interior rank)", fake), ("no neighbours", [])]
