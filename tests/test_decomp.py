@@ -278,3 +278,18 @@ def test_peer_fused_dycore_multiprocess(nproc, steps):
            str(repo / "tools" / "peer_fused_check.py"), str(steps)]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=400, cwd=str(repo))
     assert r.returncode == 0 and r.stdout.count("FUSED_PEER_OK") == nproc, (r.stdout[-2000:], r.stderr[-3000:])
+
+
+def test_peer_fused_step_needs_mirrored_build():
+    """PeerFusedStep refuses a stencil built without gen_options mirror (its
+    column kernel would not store into the neighbours' halos)."""
+    import paper_2311_08322_b200 as b200
+    from paper_2311_08322_b200 import decomp, workloads
+
+    st = b200.compile_stencil(workloads.source("dycore"), "dycore")
+    d = decomp.Decomposition((8, 8, 4), (1, 1), 0)
+    with pytest.raises(ValueError, match="mirror"):
+        decomp.PeerFusedStep(st, d, [{}], {}, "u_out", (2, 2))
+    assert st.build_info["module"]._mirror_fn is None
+    sm = b200.compile_stencil(workloads.source("dycore"), "dycore", gen_options={"mirror": "u_out"})
+    assert sm.build_info["module"]._mirror_fn is not None
