@@ -293,3 +293,53 @@ def test_peer_fused_step_needs_mirrored_build():
     assert st.build_info["module"]._mirror_fn is None
     sm = b200.compile_stencil(workloads.source("dycore"), "dycore", gen_options={"mirror": "u_out"})
     assert sm.build_info["module"]._mirror_fn is not None
+
+
+@pytest.mark.gpu
+def test_mirror_stores_exact_cells_single_process():
+    """gen_options mirror on one GPU: 8 boxes (the 2-deep faces and corners of
+    the domain) pointed at a scratch field with the identity mapping; after
+    one dycore step the scratch holds exactly u_out on the boxes' cells and is
+    untouched elsewhere (bitwise), and u_out is the plain build's."""
+    import numpy as np
+
+    import paper_2311_08322_b200 as b200
+    from paper_2311_08322_b200 import native, workloads
+
+    dom = (37, 70, 9)
+    arr = workloads.dycore_arrays(dom, 5)
+    sc = workloads.DYCORE_SCALARS
+    coef = {n: b200.from_array(arr[n]) for n in "abc"}
+    st_m = b200.compile_stencil(workloads.source("dycore"), "dycore", gen_options={"mirror": "u_out"})
+    st_p = b200.compile_stencil(workloads.source("dycore"), "dycore")
+    u = b200.from_array(arr["u"], (2, 2, 0))
+    out_m, out_p = b200.from_array(arr["u"], (2, 2, 0)), b200.from_array(arr["u"], (2, 2, 0))
+    scratch = b200.from_array(np.full_like(arr["u"], -7.0), (2, 2, 0))
+    ni, nj, _ = dom
+    org = sum(o * s for o, s in zip(scratch.origin, scratch.strides)) * scratch.itemsize
+    boxes = []
+    for di in (-1, 0, 1):
+        for dj in (-1, 0, 1):
+            if di == dj == 0:
+                continue
+            i0, i1 = {-1: (0, 2), 0: (0, ni), 1: (ni - 2, ni)}[di]
+            j0, j1 = {-1: (0, 2), 0: (0, nj), 1: (nj - 2, nj)}[dj]
+            boxes.append((i0, i1, j0, j1, scratch.base_address() + org, *scratch.strides))
+    mod = st_m.build_info["module"]
+    try:
+        mod.set_mirror(boxes)
+        st_m(u_in=u, u_out=out_m, **coef, **sc)
+    finally:
+        mod.set_mirror([])
+    st_p(u_in=u, u_out=out_p, **coef, **sc)
+    native.synchronize(native.default_stream())
+    scratch.mark_device_written()
+    got_out, want_out = out_m.host_array(), out_p.host_array()
+    assert np.array_equal(got_out, want_out)
+    s = scratch.host_array()[2:-2, 2:-2, :]
+    o = got_out[2:-2, 2:-2, :]
+    band = np.zeros(dom, bool)
+    band[:2], band[-2:], band[:, :2], band[:, -2:] = True, True, True, True
+    assert np.array_equal(s[band], o[band])
+    assert np.all(s[~band] == -7.0)
+    assert np.all(scratch.host_array()[:2] == -7.0) and np.all(scratch.host_array()[:, :2] == -7.0)
