@@ -947,7 +947,7 @@ def _emit_variant(kname, plan, sp: ThomasSpec, v: Variant, ctype, dtypes, opts):
     if _MIRROR:
         # gen_options mirror: the tile's columns that lie in a neighbour's halo
         # (up to 3: i-face, j-face, corner) send their finished column of the
-        # mirrored field there (peer stores), re-read from this thread's own
+        # mirrored field there (peer stores), re-read from the tile's own
         # stores; kept out of the level loops so they keep their registers
         t_ = ctype[_MIRROR]
         w("      {")
@@ -964,21 +964,46 @@ def _emit_variant(kname, plan, sp: ThomasSpec, v: Variant, ctype, dtypes, opts):
         w("            ++nm_;")
         w("          }")
         w("        }")
-        w("        if (nm_ > 0) {")
-        w(f"          const {t_}* src_ = colp_{_MIRROR};")
-        w(f"          const long long sk_ = p.f_{_MIRROR}.sk;")
-        MB = int((opts or {}).get("mirror_batch", 16))
-        w(f"          // {MB} levels in flight per batch (all loads, then all stores), running pointers")
-        w(f"          for (int kb = 0; kb < nk; kb += {MB}) {{")
-        w(f"            {t_} v_[{MB}];")
+        # lane-parallel over levels: the warp takes its boundary columns up to 8
+        # at a time, every lane loads levels lane, lane+32, lane+64 of each
+        # (one round of independent loads), then stores them to the targets
+        w(f"        const {t_}* const src_ = colp_{_MIRROR};")
+        w(f"        const long long sk_ = p.f_{_MIRROR}.sk;")
+        w("        __syncwarp();  // the column owners' stores before other lanes re-read them")
+        w("        unsigned bm_ = __ballot_sync(0xffffffffu, nm_ > 0);")
+        w("        while (bm_) {")
+        w("          int cl_[8];")
+        w("          #pragma unroll")
+        w("          for (int c = 0; c < 8; ++c) { cl_[c] = bm_ ? __ffs(bm_) - 1 : -1; bm_ &= bm_ ? bm_ - 1 : 0u; }")
+        w("          for (int k0 = 0; k0 < nk; k0 += 96) {")
+        w(f"            {t_} v_[8][3];")
         w("            #pragma unroll")
-        w(f"            for (int u = 0; u < {MB}; ++u) {{ if (kb + u < nk) v_[u] = *src_; src_ += sk_; }}")
+        w("            for (int c = 0; c < 8; ++c) {")
+        w("              if (cl_[c] < 0) break;")
+        w(f"              const {t_}* const s_ = ({t_}*)__shfl_sync(0xffffffffu, (unsigned long long)src_, cl_[c]);")
+        w("              #pragma unroll")
+        w("              for (int m = 0; m < 3; ++m) {")
+        w("                const int k = k0 + lane + 32 * m;")
+        w("                if (k < nk) v_[c][m] = s_[(long long)k * sk_];")
+        w("              }")
+        w("            }")
         w("            #pragma unroll")
-        w(f"            for (int u = 0; u < {MB}; ++u) {{")
-        w("              if (kb + u >= nk) break;")
-        w("              *mp0_ = v_[u]; mp0_ += mk0_;")
-        w("              if (mp1_) { *mp1_ = v_[u]; mp1_ += mk1_; }")
-        w("              if (mp2_) { *mp2_ = v_[u]; mp2_ += mk2_; }")
+        w("            for (int c = 0; c < 8; ++c) {")
+        w("              if (cl_[c] < 0) break;")
+        w(f"              {t_}* const q0_ = ({t_}*)__shfl_sync(0xffffffffu, (unsigned long long)mp0_, cl_[c]);")
+        w(f"              {t_}* const q1_ = ({t_}*)__shfl_sync(0xffffffffu, (unsigned long long)mp1_, cl_[c]);")
+        w(f"              {t_}* const q2_ = ({t_}*)__shfl_sync(0xffffffffu, (unsigned long long)mp2_, cl_[c]);")
+        w("              const long long m0_ = __shfl_sync(0xffffffffu, mk0_, cl_[c]);")
+        w("              const long long m1_ = __shfl_sync(0xffffffffu, mk1_, cl_[c]);")
+        w("              const long long m2_ = __shfl_sync(0xffffffffu, mk2_, cl_[c]);")
+        w("              #pragma unroll")
+        w("              for (int m = 0; m < 3; ++m) {")
+        w("                const long long k = k0 + lane + 32 * m;")
+        w("                if (k >= nk) break;")
+        w("                q0_[k * m0_] = v_[c][m];")
+        w("                if (q1_) q1_[k * m1_] = v_[c][m];")
+        w("                if (q2_) q2_[k * m2_] = v_[c][m];")
+        w("              }")
         w("            }")
         w("          }")
         w("        }")
