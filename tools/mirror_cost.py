@@ -52,6 +52,8 @@ def timed(boxes):
     return statistics.median(out)
 
 
+if "--sk0" in sys.argv:  # diagnostic: every level to one target plane (1 page per column instead of 80)
+    fake = [b[:7] + (0,) for b in fake]
 if "--eager" in sys.argv:  # profiler runs: a few plain steps with the 8 boxes, no graph
     step._boxes = [fake, fake]
     for _ in range(4):
