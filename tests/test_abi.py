@@ -155,3 +155,27 @@ def test_f32_exact_literals():
     assert _f32_exact_literal(0.0) and _f32_exact_literal(4.0) and _f32_exact_literal(-0.5)
     assert not _f32_exact_literal(0.1) and not _f32_exact_literal(1e300)
     assert not _f32_exact_literal(float("nan")) and not _f32_exact_literal(float("inf"))
+
+
+def test_bench_reference_arm_contract():
+    """bench.py --impl reference (the reference's own CPU kernel, oracle/_ref,
+    on the host cores): one JSON line with the arm's keys, e2e with zero
+    host<->device bytes, and the arena-reuse secondary row."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    repo = Path(__file__).resolve().parent.parent
+    if not (repo / "oracle" / "_ref" / "manifest.json").exists():
+        pytest.skip("oracle/_ref not built (run __graft_entry__.build())")
+    r = subprocess.run([sys.executable, str(repo / "bench.py"), "--impl", "reference", "--steps", "2",
+                        "--warmup", "1"], capture_output=True, text=True, timeout=300, cwd=str(repo))
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference" and line["metric"] == "grid-points/s" and line["higher_is_better"] is True
+    assert line["steps"] == 2 and line["value"] > 0
+    cb = line["cpu_baseline"]
+    assert cb["kind"] == "reference" and cb["cores"] >= 1 and cb["value"] == line["value"] and cb["sample"]
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["d2h_bytes_per_step"] == 0
+    assert cb["rows"]["gen_arena_reuse"]["value"] > 0
