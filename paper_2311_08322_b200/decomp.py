@@ -554,6 +554,18 @@ def mirror_boxes(decomp: Decomposition, halo: tuple) -> list:
     return out
 
 
+def mirror_descriptor(me: Decomposition, nb: Decomposition, box: tuple, nb_base: int, nb_strides: tuple,
+                      nb_origin: tuple, itemsize: int) -> tuple:
+    """One ``Module.set_mirror`` box: our local cells ``box`` = (i0, i1, j0, j1)
+    go to the neighbour's storage (element [0,0,0] at ``nb_base``, element
+    strides ``nb_strides``, compute-domain origin ``nb_origin``): local (i, j, k)
+    -> neighbour storage element origin + (I0 - nI0 + i, J0 - nJ0 + j, k)."""
+    si, sj, sk = nb_strides
+    oi, oj, ok = nb_origin
+    off = (oi + me.i0 - nb.i0) * si + (oj + me.j0 - nb.j0) * sj + ok * sk
+    return (*box, nb_base + off * itemsize, si, sj, sk)
+
+
 class PeerFusedStep:
     """One decomposed time step in ONE kernel launch: the producing kernel
     itself stores the boundary values of its output into the neighbours'
@@ -640,15 +652,13 @@ class PeerFusedStep:
         # per phase: the mirror boxes into the neighbours' copy of that phase's output
         self._boxes, self._launch = [], []
         item = outs[0].itemsize
-        I0, J0 = decomposition.i0, decomposition.j0
         for ph in phases:
             oi = next(x for x, f in enumerate(outs) if f is ph[out_field])
             boxes = []
-            for d, nb, (bi0, bi1, bj0, bj1) in self.neighbours:
-                base, (si, sj, sk), (oi_, oj_, ok_), (nI0, nJ0) = remote_outs[(d, oi)]
-                # our local (i, j) -> neighbour storage element origin + (I0 - nI0 + i, J0 - nJ0 + j)
-                off = (oi_ + I0 - nI0) * si + (oj_ + J0 - nJ0) * sj + ok_ * sk
-                boxes.append((bi0, bi1, bj0, bj1, base + off * item, si, sj, sk))
+            for d, nb, box in self.neighbours:
+                base, strides, origin, _ = remote_outs[(d, oi)]
+                nbd = Decomposition(decomposition.global_domain, decomposition.grid, nb)
+                boxes.append(mirror_descriptor(decomposition, nbd, box, base, strides, origin, item))
             self._boxes.append(boxes)
             self._launch.append(module.launcher(dom, ph, scalars, self.stream))
         self._step = 0

@@ -343,3 +343,48 @@ def test_mirror_stores_exact_cells_single_process():
     assert np.array_equal(s[band], o[band])
     assert np.all(s[~band] == -7.0)
     assert np.all(scratch.host_array()[:2] == -7.0) and np.all(scratch.host_array()[:, :2] == -7.0)
+
+
+@pytest.mark.parametrize("grid", [(2, 2), (3, 3), (4, 2)])
+def test_mirror_descriptors_fill_halos_on_host(grid):
+    """decomp.mirror_descriptor addressing, emulated with numpy: every rank
+    stores its boxes' cells through the descriptors (base + i*s_i + j*s_j +
+    k*s_k) into its neighbours' storages; afterwards every halo cell inside
+    the global domain holds the global value, every other halo cell is
+    untouched."""
+    import numpy as np
+
+    from paper_2311_08322_b200 import decomp
+
+    gdom = (7 * grid[0] + 3, 9 * grid[1] + 2, 3)
+    rng = np.random.default_rng(3)
+    g = rng.uniform(-1, 1, gdom)
+    ds = [decomp.Decomposition(gdom, grid, r) for r in range(grid[0] * grid[1])]
+    st = {}
+    for d in ds:
+        ni, nj, nk = d.local_domain
+        a = np.full((ni + 4, nj + 4, nk), np.nan)
+        a[2:-2, 2:-2] = g[d.i0:d.i1, d.j0:d.j1]
+        st[d.rank] = a
+    item = 8
+    for d in ds:
+        for _, nb, box in decomp.mirror_boxes(d, (2, 2)):
+            dst = st[nb]
+            strides = tuple(s // item for s in dst.strides)
+            desc = decomp.mirror_descriptor(d, ds[nb], box, 0, strides, (2, 2, 0), item)
+            i0, i1, j0, j1, base, si, sj, sk = desc
+            flat = dst.reshape(-1)
+            for i in range(i0, i1):
+                for j in range(j0, j1):
+                    for k in range(gdom[2]):
+                        flat[base // item + i * si + j * sj + k * sk] = st[d.rank][2 + i, 2 + j, k]
+    for d in ds:
+        a = st[d.rank]
+        for li in range(a.shape[0]):
+            for lj in range(a.shape[1]):
+                gi, gj = d.i0 + li - 2, d.j0 + lj - 2
+                inside = 0 <= gi < gdom[0] and 0 <= gj < gdom[1]
+                if inside:
+                    assert np.array_equal(a[li, lj], g[gi, gj]), (d.rank, li, lj)
+                else:
+                    assert np.all(np.isnan(a[li, lj])), (d.rank, li, lj)
