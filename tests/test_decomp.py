@@ -388,3 +388,44 @@ def test_mirror_descriptors_fill_halos_on_host(grid):
                     assert np.array_equal(a[li, lj], g[gi, gj]), (d.rank, li, lj)
                 else:
                     assert np.all(np.isnan(a[li, lj])), (d.rank, li, lj)
+
+
+@pytest.mark.parametrize("nranks", [2, 3, 4])
+def test_fused_step_protocol_model(nranks):
+    """The PeerFusedStep step protocol (one arrival counter per neighbour,
+    initialised to 1; per step: wait until every neighbour's counter reaches
+    the step count + 1, run the kernel, bump every neighbour's counter), model
+    checked on a chain of ranks over many random schedules: a kernel never
+    writes a neighbour's halo while that neighbour's kernel reads it, and
+    every halo a kernel reads was written by the neighbours' previous step."""
+    import random
+
+    steps = 6
+    nbs = {r: [n for n in (r - 1, r + 1) if 0 <= n < nranks] for r in range(nranks)}
+    for seed in range(300):
+        rnd = random.Random(seed)
+        arrived = {r: {n: 1 for n in nbs[r]} for r in range(nranks)}  # arrivals at r from n
+        step = {r: 0 for r in range(nranks)}
+        state = {r: "wait" for r in range(nranks)}  # wait -> run -> (signal) -> wait
+        halo_written = {(r, b): {n: -1 for n in nbs[r]} for r in range(nranks) for b in (0, 1)}
+        while any(step[r] < steps for r in range(nranks)):
+            r = rnd.choice([x for x in range(nranks) if step[x] < steps])
+            s = step[r]
+            if state[r] == "wait":
+                if all(arrived[r][n] >= s + 1 for n in nbs[r]):
+                    state[r] = "run"
+                    # the kernel reads buffer s % 2's halo: written by each neighbour's step s-1
+                    for n in nbs[r]:
+                        assert s == 0 or halo_written[(r, s % 2)][n] == s - 1, (seed, r, s, n)
+            else:  # "run": the kernel writes neighbours' buffer (s+1) % 2 halo, then signals
+                for n in nbs[r]:
+                    # n must not be running a step that reads buffer (s+1) % 2, i.e. s-1 or s+1
+                    assert not (state[n] == "run" and step[n] in (s - 1, s + 1)), (seed, r, s, n, step[n])
+                    halo_written[(n, (s + 1) % 2)][r] = s
+                    arrived[n][r] += 1
+                state[r] = "wait"
+                step[r] += 1
+            # writer (step s, anywhere in its run) and reader (step s +- 1) never overlap
+            for x in range(nranks):
+                for n in nbs[x]:
+                    assert not (state[x] == "run" and state[n] == "run" and abs(step[x] - step[n]) == 1), seed
