@@ -56,6 +56,29 @@ sd(u_in=u_in, u_out=u_out, **{n: b200.from_array(arr[n]) for n in "abc"}, **work
 check("dycore", u_out.host_array()[2:-2, 2:-2, :],
       oracle.dycore_step(arr["u"], arr["a"], arr["b"], arr["c"], **workloads.DYCORE_SCALARS))
 
+# the dycore with mirrored halo stores (gen_options mirror; PeerFusedStep's
+# kernel): the 8 boxes of an interior rank pointed at a scratch field
+sm = b200.compile_stencil(workloads.source("dycore"), "dycore", gen_options={"mirror": "u_out"})
+u_out2 = b200.from_array(arr["u"], (2, 2, 0))
+scratch = b200.from_array(np.zeros_like(arr["u"]), (2, 2, 0))
+org = sum(o * st_ for o, st_ in zip(scratch.origin, scratch.strides)) * scratch.itemsize
+mboxes = []
+for di in (-1, 0, 1):
+    for dj in (-1, 0, 1):
+        if di or dj:
+            bi = {-1: (0, 2), 0: (0, ddom[0]), 1: (ddom[0] - 2, ddom[0])}[di]
+            bj = {-1: (0, 2), 0: (0, ddom[1]), 1: (ddom[1] - 2, ddom[1])}[dj]
+            mboxes.append((*bi, *bj, scratch.base_address() + org, *scratch.strides))
+sm.build_info["module"].set_mirror(mboxes)
+sm(u_in=u_in, u_out=u_out2, **{n: b200.from_array(arr[n]) for n in "abc"}, **workloads.DYCORE_SCALARS)
+sm.build_info["module"].set_mirror([])
+native.synchronize(native.default_stream())
+scratch.mark_device_written()
+band = np.zeros(ddom, bool)
+band[:2], band[-2:], band[:, :2], band[:, -2:] = True, True, True, True
+check("dycore mirrored", np.where(band, scratch.host_array()[2:-2, 2:-2, :], u_out2.host_array()[2:-2, 2:-2, :]),
+      oracle.dycore_step(arr["u"], arr["a"], arr["b"], arr["c"], **workloads.DYCORE_SCALARS))
+
 # halo pack / unpack and the peer copy-box kernel on one device
 f = b200.from_array(rng.uniform(-1, 1, (12, 9, 4)), (2, 2, 0))
 g = b200.allocate("f64", (8, 5, 4), (2, 2, 0))
