@@ -5,8 +5,9 @@
 
 Fused PARALLEL tile kernel (hdiff f64 / f32), TMEM column kernels (vadv: W=2
 at nk=20, W=1 at nk=120, generic column kernel at nk=200), the fused dycore
-column kernel, per-stage / plane fallbacks (fuse_parallel off), halo pack /
-unpack and the peer copy-box kernel."""
+column kernel and its mirrored-halo build (gen_options mirror), per-stage /
+plane fallbacks (fuse_parallel off), halo pack / unpack and the peer copy-box
+kernel."""
 import sys
 from pathlib import Path
 
