@@ -46,6 +46,8 @@ WORKLOADS = {
     "hdiff32": ("hdiff", "f32", (256, 256, 80)),
     "vadv32": ("vadv", "f32", (256, 256, 80)),
 }
+SHORT_TEXT = {"vadv": "vadv 256x256x80 f64", "hdiff": "hdiff 256x256x80 f64", "hdiff32": "hdiff 256x256x80 f32",
+              "vadv32": "vadv 256x256x80 f32"}
 CONFIG_TEXT = {
     "vadv": "vertical advection (FORWARD/BACKWARD Thomas) 256x256x80 float64",
     "hdiff": "horizontal diffusion 256x256x80 float64",
@@ -361,6 +363,13 @@ def ncu_traffic(workload: str):
     return None
 
 
+def _traffic_bytes(workload: str):
+    """DRAM read + write bytes per launch of the workload's kernel from the
+    committed ``ncu --set full`` capture (profiles/ncu_traffic.json)."""
+    t = ncu_traffic(workload)
+    return None if not t else t.get("traffic_bytes")
+
+
 def device_timed(st, kernel, dtype, domain, steps, warmup, dist, sampler=None, use_graph=True):
     """Device-resident timing with rotating buffer sets."""
     from paper_2311_08322_b200 import native, workloads
@@ -395,9 +404,11 @@ def device_timed(st, kernel, dtype, domain, steps, warmup, dist, sampler=None, u
         # kernels costs ~5 us, more than a 256^2 hdiff's own ramp; the mean
         # launch duration is the timed region / K, gaps included)
         graph = native.Graph(stream)
+        n0 = module.launch_count()
         with graph.capture():
             for i in range(steps):
                 launchers[(warmup + i) % nsets]()
+        n_launch = module.launch_count() - n0
         graph.launch()
         native.synchronize(stream)
         dist.barrier()
@@ -406,12 +417,15 @@ def device_timed(st, kernel, dtype, domain, steps, warmup, dist, sampler=None, u
         if graph is not None:
             graph.launch()
         else:
+            n0 = module.launch_count()
             for i in range(steps):
                 ev[i][0].record(stream)
                 launchers[(warmup + i) % nsets]()
                 ev[i][1].record(stream)
         e1.record(stream)
         native.synchronize(stream)
+        if graph is None:
+            n_launch = module.launch_count() - n0
     dist.barrier()
     total_ms = e0.elapsed_ms(e1)
     if graph is not None:
@@ -421,7 +435,7 @@ def device_timed(st, kernel, dtype, domain, steps, warmup, dist, sampler=None, u
     return {"total_ms": total_ms, "launch_ms_mean": statistics.fmean(launch_ms),
             "launch_ms_median": statistics.median(launch_ms), "nsets": nsets,
             "set_mb": set_bytes / 1e6, "l2_mb": info["l2_bytes"] / 1e6, "sets": sets,
-            "launches_per_step": sum(1 for k in module.plan.kernels),
+            "launches": n_launch, "launches_per_step": n_launch / steps,
             "launch": ("cuda graph of the K timed steps; kernel time = timed region / K" if graph is not None
                        else "eager; kernel time = mean of per-launch event pairs")}
 
@@ -435,29 +449,47 @@ class _Null:
 
 
 def parity_check(kernel, dtype, sets):
-    """Verify the last buffer set against the C oracle (bitwise)."""
+    """The first buffer set vs the C oracle AND the reference gen engine's
+    own kernel (oracle/_ref) on the same inputs: "bitwise" when both agree
+    bit for bit."""
     sys.path.insert(0, str(REPO / "oracle"))
     import oracle
 
     a = sets[0]
     if kernel == "hdiff":
-        want = oracle.hdiff_c(a["inp"].host_array(), a["coeff"])
+        ins = (a["inp"].host_array(), a["coeff"])
         got = a["out"].host_array()
+        checks = [("oracle", oracle.hdiff_c)] + ([("ref", oracle.ref_hdiff)]
+                                                 if oracle.ref_available(f"hdiff_{dtype}") else [])
     else:
-        want = oracle.vadv_c(*[a[n].host_array() for n in "abcd"])
+        ins = tuple(a[n].host_array() for n in "abcd")
         got = a["x"].host_array()
-    return "bitwise" if np.array_equal(got, want) else f"max_rel {oracle.max_rel(got, want):.3e}"
+        checks = [("oracle", oracle.vadv_c)] + ([("ref", oracle.ref_vadv)]
+                                                if oracle.ref_available(f"vadv_{dtype}") else [])
+    bad = []
+    for name, fn in checks:
+        want = fn(*ins)
+        if not np.array_equal(got, want):
+            bad.append(f"{name} max_rel {oracle.max_rel(got, want):.2e}")
+    if bad:
+        return "; ".join(bad)
+    return "bitwise(" + "+".join(n for n, _ in checks) + ")"
 
 
-def e2e_timed(st, kernel, dtype, domain, steps):
-    """Through CompiledStencil.__call__ with pinned host FieldStorages."""
+def e2e_timed(st, kernel, dtype, domain, steps, pinned=True):
+    """Through CompiledStencil.__call__ with HOST FieldStorages: the
+    reference's own storages from its harness builder (make_<kernel>_args with
+    the b200 layout: pageable numpy memory, stencilforge bench.py:82-105), or
+    the same values in page-locked storages (storage.pinned_host_storage).
+    Every call copies its inputs host -> device and its outputs back."""
+    from paper_2311_08322_b200 import backend as b2b
     from paper_2311_08322_b200 import storage as b2s
     from paper_2311_08322_b200 import workloads
 
     host = workloads.make_args(kernel, domain, dtype, device=False)
     args = {}
     for n, v in host.items():
-        if hasattr(v, "base_address"):
+        if hasattr(v, "base_address") and pinned:
             halo = v.origin
             comp = tuple(s - 2 * h for s, h in zip(v.shape, halo))
             p = b2s.pinned_host_storage(v.dtype, comp, halo)
@@ -465,28 +497,30 @@ def e2e_timed(st, kernel, dtype, domain, steps):
             args[n] = p
         else:
             args[n] = v
-    from paper_2311_08322_b200 import backend as b2b
-
     st(**args)  # warm (allocates the device mirrors)
     t0 = time.perf_counter()
     for _ in range(steps):
         st(**args)
     dt = (time.perf_counter() - t0) / steps
-    tr = dict(b2b.last_transfer)  # bytes the last call actually moved
+    tr = dict(b2b.call_stats())  # bytes the last call actually moved
     return dt, tr["h2d"], tr["d2h"], tr["chunks"]
 
 
-def decomposed_hdiff(dist, steps, warmup, tile=(512, 1024, 80), transport="nccl"):
+def decomposed_hdiff(dist, steps, warmup, tile=(512, 1024, 80), transport="nccl", split=None):
     """C4: hdiff on a horizontally decomposed domain, a fixed 512x1024x80
-    tile per GPU (weak scaling; 2048x2048x80 at 8 GPUs on a 4x2 grid); each
-    step = NCCL halo exchange of inp overlapped with the interior + boundary
-    strips.  Returns (max-over-ranks ms per step, global domain, grid)."""
+    tile per GPU (weak scaling; 2048x2048x80 at 8 GPUs on a 4x2 grid).  Each
+    step = the halo exchange of inp (``nccl``: NCCL send/recv; ``peer``: CUDA
+    IPC peer stores + flags) overlapped with the interior, then the boundary
+    frame (decomp.DecomposedStep: 2 launches per step); ``none``: the tile
+    alone, as at N=1.  The timed steps are replayed from one CUDA graph (the
+    NCCL calls are captured too).  Returns (max-over-ranks ms per step,
+    global domain, grid, launches per step)."""
     import paper_2311_08322_b200 as b200
     from paper_2311_08322_b200 import decomp, native, workloads
 
-    grid = decomp.choose_grid(dist.world)
+    grid = decomp.choose_grid(dist.world) if transport != "none" else (1, 1)
     gdom = (tile[0] * grid[0], tile[1] * grid[1], tile[2])
-    d = decomp.Decomposition(gdom, grid, dist.rank)
+    d = decomp.Decomposition(gdom, grid, dist.rank if transport != "none" else 0)
     ldom = d.local_domain
     st = b200.compile_stencil(workloads.source("hdiff"), "hdiff")
     rng = np.random.default_rng(1000 + dist.rank)
@@ -495,34 +529,59 @@ def decomposed_hdiff(dist, steps, warmup, tile=(512, 1024, 80), transport="nccl"
     if transport == "peer":
         step = decomp.PeerDecomposedStep(st, d, {"inp": inp, "out": out}, {"coeff": 0.05}, "inp", (2, 2))
     else:
-        step = decomp.DecomposedStep(st, d, {"inp": inp, "out": out}, {"coeff": 0.05}, "inp", (2, 2))
-    stream = native.default_stream()
+        step = decomp.DecomposedStep(st, d, {"inp": inp, "out": out}, {"coeff": 0.05}, "inp", (2, 2),
+                                     split=split)
+    stream = step.stream if hasattr(step, "stream") else step.compute
     for _ in range(warmup):
         step()
     native.synchronize(stream)
-    replay = None
-    if transport == "peer":
-        replay = step.graph(steps)  # no NCCL call: capturable
-    elif dist.world == 1:  # no exchange at all: the launches alone, captured like the headline
-        g = native.Graph(stream)
-        with g.capture():
-            for _ in range(steps):
-                step()
-        replay = g
+    module = st.build_info["module"]
+    n0 = module.launch_count()
+    replay = step.graph(steps)
+    lps = (module.launch_count() - n0) / steps
+    replay.launch()  # upload + warm replay
+    native.synchronize(stream)
     e0, e1 = native.Event(), native.Event()
     dist.barrier()
     native.synchronize(stream)
     e0.record(stream)
-    if replay is not None:
-        replay.launch()
-    else:
-        for _ in range(steps):
-            step()
+    replay.launch()
     e1.record(stream)
     native.synchronize(stream)
     dist.barrier()
     ms = dist.max(e0.elapsed_ms(e1) / steps)
-    return ms, gdom, grid, step.launches_per_step
+    if hasattr(step, "close"):
+        step.close()
+    return ms, gdom, grid, lps
+
+
+def c4_weak_scaling(dist, args, tile=(512, 1024, 80)):
+    """BASELINE configs[3] / north_star scaling target: hdiff f64 with a fixed
+    512x1024x80 tile per GPU on the rank grid (1x1, 2x1, 2x2, 4x2 -> 2048x
+    2048x80 at 8 GPUs).  Measured in this run: the tile alone (no neighbours,
+    ``tile_us``, every rank), then the decomposed step over the NCCL transport
+    and (N > 1) the peer-memory transport; efficiency = tile time / step time
+    (weak scaling, max over ranks)."""
+    nst = max(args.steps // 4, 20)
+    out: dict = {"tile": list(tile), "gpus": dist.world}
+    ms1, _, _, lps1 = decomposed_hdiff(dist, nst, args.warmup, tile=tile, transport="none")
+    out["tile_us"] = ms1 * 1e3
+    out["tile_launches_per_step"] = lps1
+    # the same tile as interior + frame launches without an exchange: what
+    # the overlap split itself costs on one GPU
+    ms_s, _, _, lps_s = decomposed_hdiff(dist, nst, args.warmup, tile=tile, transport="none", split=True)
+    out["split_us"] = ms_s * 1e3
+    out["split_launches_per_step"] = lps_s
+    transports = ("nccl", "peer") if dist.world > 1 and not dist.shared else ()
+    for tr in transports:
+        try:
+            ms, gdom, grid, lps = decomposed_hdiff(dist, nst, args.warmup, tile=tile, transport=tr)
+            out["grid"], out["global"] = list(grid), list(gdom)
+            out[tr] = {"us_per_step": ms * 1e3, "efficiency": ms1 / ms, "launches_per_step": lps,
+                       "value": gdom[0] * gdom[1] * gdom[2] / (ms / 1e3)}
+        except Exception as exc:  # reported, not fatal
+            out[tr] = {"error": f"{type(exc).__name__}: {exc}"[:200]}
+    return out
 
 
 def dycore_decomposed_peer(dist, steps=20, tile=(512, 512, 80)):
@@ -610,12 +669,14 @@ def dycore_fused_peer(dist, steps=20, tile=(512, 512, 80)):
             "launches_per_step": 3 if dist.world > 1 else 1}
 
 
-def dycore_timed(dist, steps=100, domain=(512, 512, 80), reps=3, gen_options=None):
+def dycore_timed(dist, steps=100, domain=(512, 512, 80), reps=3, gen_options=None, check=True):
     """BASELINE.json configs[4]: the dycore-like step (kernels/dycore.gts:
     hdiff -> Thomas solve -> interval-specialised update) on 512x512x80 f64,
-    ``steps`` time steps per run captured in one CUDA graph (TimeLoop); one
-    untimed warm-up replay, then ``reps`` timed replays (CUDA events, max over
-    ranks).  Inputs (1.4 GB of fields + temporaries) exceed the L2 16x."""
+    ``steps`` time steps per run captured in one CUDA graph (TimeLoop).  The
+    first replay (the first ``steps`` steps from the initial state, untimed)
+    is checked bitwise against the reference gen engine's own dycore kernel
+    (oracle/_ref, ``steps`` host-swapped calls); then ``reps`` timed replays
+    (CUDA events, max over ranks).  Fields + temporaries exceed the L2 16x."""
     import paper_2311_08322_b200 as b200
     from paper_2311_08322_b200 import native, workloads
     from paper_2311_08322_b200.timeloop import TimeLoop
@@ -627,7 +688,19 @@ def dycore_timed(dist, steps=100, domain=(512, 512, 80), reps=3, gen_options=Non
     loop = TimeLoop(st, [dict(u_in=A, u_out=B, **coef), dict(u_in=B, u_out=A, **coef)], steps,
                     workloads.DYCORE_SCALARS)
     stream = loop.stream
-    loop.run()  # capture + warm-up replay
+    loop.run()  # capture + the first `steps` steps
+    parity = None
+    if check:
+        sys.path.insert(0, str(REPO / "oracle"))
+        import oracle
+
+        got = (A, B)[steps % 2].host_array()
+        if oracle.ref_available("dycore_f64"):
+            want = oracle.ref_dycore_run(arr["u"], arr["a"], arr["b"], arr["c"], steps)
+            parity = (f"bitwise(ref,{steps} steps)" if np.array_equal(got, want)
+                      else f"ref max_rel {oracle.max_rel(got, want):.2e}")
+        else:
+            parity = "finite" if np.isfinite(got).all() else "NON-FINITE"
     e0, e1 = native.Event(), native.Event()
     dist.barrier()
     native.synchronize(stream)
@@ -640,18 +713,35 @@ def dycore_timed(dist, steps=100, domain=(512, 512, 80), reps=3, gen_options=Non
     ms = dist.max(e0.elapsed_ms(e1) / reps)
     pts = domain[0] * domain[1] * domain[2]
     alg = workloads.algorithmic_bytes("dycore", domain)
-    # parity spot check of the first replay against the oracle is done by
-    # tests/test_dycore.py; here: the state stays finite after 400 steps
-    final = A.host_array()
     return {
-        "workload": f"dycore step (kernels/dycore.gts: hdiff -> Thomas -> interval-specialised update) "
-                    f"{domain[0]}x{domain[1]}x{domain[2]} float64, {steps} time steps per CUDA-graph replay",
         "value": dist.world * pts * steps / (ms / 1e3), "unit": "grid-point-steps/s",
-        "ms_per_step": ms / steps, "ms_per_100_steps": ms * 100 / steps,
-        "achieved_gbs": alg / (ms / steps / 1e3) / 1e9,
-        "algorithmic_bytes_per_step": alg, "plan": st.build_info["plan"],
-        "launches_per_step": loop.launches_per_step, "finite": bool(np.isfinite(final).all()),
+        "us_per_step": 1e3 * ms / steps, "achieved_gbs": alg / (ms / steps / 1e3) / 1e9,
+        "launches_per_step": loop.launches_per_step, "parity": parity,
     }
+
+
+def _r(x, n=4):
+    """Round for the compact JSON line."""
+    if isinstance(x, float):
+        return float(f"{x:.{n}g}")
+    if isinstance(x, dict):
+        return {k: _r(v, n) for k, v in x.items()}
+    if isinstance(x, list):
+        return [_r(v, n) for v in x]
+    return x
+
+
+def _extra_guard(fn, *a, **k):
+    try:
+        return fn(*a, **k)
+    except Exception as exc:  # pragma: no cover - reported, not fatal
+        return {"error": f"{type(exc).__name__}: {exc}"[:200]}
+
+
+def _detail_path(dist) -> Path:
+    d = REPO / "gpurun_out"
+    d.mkdir(exist_ok=True)
+    return d / f"bench_detail_n{dist.world}.json"
 
 
 def run_b200(args, dist):
@@ -676,33 +766,31 @@ def run_b200(args, dist):
     peak, peak_src = measured_peak()
     alg = workloads.algorithmic_bytes(kernel, domain, dtype)
     achieved = alg / (launch_ms / 1e3) / 1e9
-    e2e_s, h2d, d2h, chunks = e2e_timed(st, kernel, dtype, domain, args.e2e_steps)
+    e2e_s, h2d, d2h, chunks = e2e_timed(st, kernel, dtype, domain, args.e2e_steps, pinned=True)
     e2e_val = dist.max(e2e_s)
+    pg_s, pg_h2d, pg_d2h, _ = e2e_timed(st, kernel, dtype, domain, max(args.e2e_steps // 2, 5), pinned=False)
+    pg_val = dist.max(pg_s)
+    detail: dict = {"device_timed": r, "peak_source": peak_src}
     line = {
-        "metric": "grid-points/s (achieved HBM GB/s in roofline)",
+        "metric": "grid-points/s",
         "value": value, "unit": "grid-points/s", "n_gpus": dist.world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": dtype,
-        "data": "synthetic (reference bench generators, seeds 0..R-1)",
-        "config": {"workload": CONFIG_TEXT[args.workload], "domain_per_gpu": list(domain),
-                   "parallelism": (f"independent column shards x{dist.world}" if dist.world > 1 else "single GPU")
-                   + (" (GTS_BENCH_SHARED_GPU: all ranks share one GPU -- a code-path check, not a scaling number)"
-                      if dist.shared and dist.world > 1 else ""),
-                   "l2": f"{r['nsets']} rotating input/output sets of {r['set_mb']:.0f} MB "
-                         f"(> 2x the {r['l2_mb']:.0f} MB L2)",
-                   "launch": r["launch"]},
+        "data": "synthetic (reference bench generators)",
+        "config": {"workload": SHORT_TEXT[args.workload], "domain_per_gpu": list(domain),
+                   "parallelism": (f"{dist.world} column shards" if dist.world > 1 else "1 GPU")
+                   + (" (shared GPU)" if dist.shared and dist.world > 1 else ""),
+                   "l2": f"{r['nsets']} rotating sets > 2x L2",
+                   "launch": "cuda graph" if not args.no_graph else "eager"},
         "parity": parity,
+        "gpu_launches": r["launches"],
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": _traffic_bytes(args.workload),
+                     "alg_bytes": alg, "kernel_us": launch_ms * 1e3},
         "e2e": {"value": dist.world * pts / e2e_val, "unit": "grid-points/s",
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-                "ms_per_step": e2e_val * 1e3,
-                "path": "CompiledStencil.__call__ with host FieldStorages (pinned), mirror mode"
-                        + (f", pipelined over {chunks} i-row chunks (H2D / kernel / D2H overlapped)"
-                           if chunks else "")},
-        "gpu_launches": args.steps * r["launches_per_step"],
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": ncu_traffic(args.workload),
-                     "algorithmic_bytes_per_launch": alg, "kernel_ms_mean": launch_ms,
-                     "peak_source": peak_src, "frac_of_8TBs_spec": achieved / 8000.0},
+                "ms": e2e_val * 1e3, "pinned": True,
+                "pageable": {"value": dist.world * pts / pg_val, "ms": pg_val * 1e3}},
         "clocks": sampler.summary(),
     }
     # Watchdog for the extras (multi-rank exchanges that have not run on this
@@ -715,131 +803,71 @@ def run_b200(args, dist):
         if not done.wait(args.extra_timeout):
             if dist.rank == 0:
                 line["extra"] = {"error": f"extras timed out after {args.extra_timeout:.0f} s"}
-                print(json.dumps(line), flush=True)
+                print(json.dumps(_r(line)), flush=True)
             os._exit(0)
 
     threading.Thread(target=_watchdog, daemon=True).start()
-    decomp_line = None
-    if dist.shared and dist.world > 1:
-        decomp_line = {"skipped": "GTS_BENCH_SHARED_GPU: NCCL cannot run two ranks on one GPU"}
-    elif not args.no_extra:
-        try:
-            ms_d, gdom, grid, lps = decomposed_hdiff(dist, max(args.steps // 4, 20), args.warmup)
-            pts_d = gdom[0] * gdom[1] * gdom[2]
-            alg_d = dist.world * workloads.algorithmic_bytes("hdiff", (512, 1024, 80), "f64")
-            decomp_line = {
-                "workload": "horizontal diffusion float64, 512x1024x80 per GPU, decomposed "
-                            f"{grid[0]}x{grid[1]} (global {gdom[0]}x{gdom[1]}x{gdom[2]}), NCCL halo "
-                            "exchange of inp overlapped with the interior"
-                            + ("; N=1: no neighbours, the timed steps replayed from one CUDA graph"
-                               if dist.world == 1 else ""),
-                "value": pts_d / (ms_d / 1e3), "unit": "grid-points/s", "ms_per_step": ms_d,
-                "achieved_gbs_per_gpu": alg_d / dist.world / (ms_d / 1e3) / 1e9,
-                "launches_per_step": lps, "scaling": "weak",
-            }
-        except Exception as exc:  # pragma: no cover - reported, not fatal
-            decomp_line = {"error": f"{type(exc).__name__}: {exc}"[:300]}
-    peer_line = None
-    if not args.no_extra and dist.world > 1:
-        try:
-            ms_p, gdom, grid, lps = decomposed_hdiff(dist, max(args.steps // 4, 20), args.warmup,
-                                                     transport="peer")
-            alg_p = workloads.algorithmic_bytes("hdiff", (512, 1024, 80), "f64")
-            peer_line = {
-                "workload": "horizontal diffusion float64, 512x1024x80 per GPU, decomposed "
-                            f"{grid[0]}x{grid[1]} (global {gdom[0]}x{gdom[1]}x{gdom[2]}), halo exchange by "
-                            "CUDA-IPC peer stores + counter flags (no NCCL), overlapped with the interior; "
-                            "the timed steps replayed from one CUDA graph",
-                "value": gdom[0] * gdom[1] * gdom[2] / (ms_p / 1e3), "unit": "grid-points/s",
-                "ms_per_step": ms_p, "achieved_gbs_per_gpu": alg_p / (ms_p / 1e3) / 1e9,
-                "launches_per_step": lps, "scaling": "weak",
-            }
-        except Exception as exc:  # pragma: no cover - reported, not fatal
-            peer_line = {"error": f"{type(exc).__name__}: {exc}"[:300]}
-    dy_peer = None
-    if not args.no_extra and dist.world > 1:
-        try:
-            dy_peer = dycore_decomposed_peer(dist)
-        except Exception as exc:  # pragma: no cover - reported, not fatal
-            dy_peer = {"error": f"{type(exc).__name__}: {exc}"[:300]}
-    dy_fused = None
-    if not args.no_extra and dist.world > 1:
-        try:
-            dy_fused = dycore_fused_peer(dist)
-        except Exception as exc:  # pragma: no cover - reported, not fatal
-            dy_fused = {"error": f"{type(exc).__name__}: {exc}"[:300]}
-    if dist.rank == 0 and dist.world > 1:
-        line["extra"] = {"hdiff_decomposed": decomp_line, "hdiff_decomposed_peer": peer_line,
-                         "dycore_decomposed_peer": dy_peer, "dycore_fused_peer": dy_fused}
+    extra: dict = {}
+    if not args.no_extra:
+        c4 = c4_weak_scaling(dist, args)
+        detail["c4"] = c4
+        if dist.world > 1:
+            line["c4"] = c4
+        else:
+            extra["c4_tile"] = c4
     if dist.rank == 0 and dist.world == 1 and not args.no_extra:
-        extra = {}
+        nst = max(args.steps // 2, 50)
         for name in ("hdiff", "hdiff32"):
             k2, d2, dom2 = WORKLOADS[name]
             st2 = b200.compile_stencil(workloads.source(k2, d2), k2)
-            r2 = device_timed(st2, k2, d2, dom2, max(args.steps // 2, 50), args.warmup, dist,
-                              use_graph=not args.no_graph)
-            alg2 = workloads.algorithmic_bytes(k2, dom2, d2)
-            ach2 = alg2 / (r2["launch_ms_mean"] / 1e3) / 1e9
-            extra[name] = {
-                "workload": CONFIG_TEXT[name],
-                "value": dom2[0] * dom2[1] * dom2[2] / (r2["total_ms"] / max(args.steps // 2, 50) / 1e3),
-                "unit": "grid-points/s", "ms_per_step": r2["total_ms"] / max(args.steps // 2, 50),
-                "kernel_ms_mean": r2["launch_ms_mean"], "achieved_gbs": ach2, "frac": ach2 / peak,
-                "parity": parity_check(k2, d2, r2["sets"]), "traffic": ncu_traffic(name),
-                "launches_per_step": r2["launches_per_step"],
-            }
-        extra["hdiff_decomposed"] = decomp_line
-        # BASELINE configs[0]: hdiff 128x128x64 f64, the reference's CPU-runnable
-        # case -- the b200 kernel and the reference gen kernel on the same inputs
-        try:
-            dom1 = (128, 128, 64)
-            st1 = b200.compile_stencil(workloads.source("hdiff", "f64"), "hdiff")
-            r1 = device_timed(st1, "hdiff", "f64", dom1, max(args.steps // 2, 50), args.warmup, dist,
-                              use_graph=not args.no_graph)
-            pts1 = dom1[0] * dom1[1] * dom1[2]
-            alg1 = workloads.algorithmic_bytes("hdiff", dom1, "f64")
-            c1 = {"workload": "horizontal diffusion 128x128x64 float64 (BASELINE configs[0])",
-                  "value": pts1 / (r1["launch_ms_mean"] / 1e3), "unit": "grid-points/s",
-                  "kernel_ms_mean": r1["launch_ms_mean"],
-                  "achieved_gbs": alg1 / (r1["launch_ms_mean"] / 1e3) / 1e9,
-                  "parity": parity_check("hdiff", "f64", r1["sets"])}
-            if not args.no_cpu_baseline:
-                t1 = time_reference("hdiff", "f64", dom1, seconds=3.0, max_calls=2000)
-                if t1:
-                    c1["cpu_reference"] = {"value": pts1 / statistics.median(t1), "unit": "grid-points/s",
-                                           "median_call_ms": statistics.median(t1) * 1e3,
-                                           "cores": host_info()[0], "calls": len(t1)}
-            extra["hdiff_c1"] = c1
-        except Exception as exc:  # pragma: no cover - reported, not fatal
-            extra["hdiff_c1"] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
-        try:
-            dy = dycore_timed(dist)
-            dy["frac"] = dy["achieved_gbs"] / peak
-            dy["traffic"] = ncu_traffic("dycore")
-            extra["dycore"] = dy
-        except Exception as exc:  # pragma: no cover - reported, not fatal
-            extra["dycore"] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
-        try:
-            extra["dycore_fused_peer"] = dycore_fused_peer(dist)
-        except Exception as exc:  # pragma: no cover - reported, not fatal
-            extra["dycore_fused_peer"] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
-        line["extra"] = extra
+            r2 = device_timed(st2, k2, d2, dom2, nst, args.warmup, dist, use_graph=not args.no_graph)
+            ach2 = workloads.algorithmic_bytes(k2, dom2, d2) / (r2["launch_ms_mean"] / 1e3) / 1e9
+            extra[name] = {"us": r2["launch_ms_mean"] * 1e3, "frac": ach2 / peak,
+                           "parity": parity_check(k2, d2, r2["sets"]),
+                           "launches_per_step": r2["launches_per_step"]}
+        # BASELINE configs[0]: hdiff 128x128x64 f64 with the reference gen
+        # kernel timed on the same inputs
+        dom1 = (128, 128, 64)
+        st1 = b200.compile_stencil(workloads.source("hdiff", "f64"), "hdiff")
+        r1 = device_timed(st1, "hdiff", "f64", dom1, nst, args.warmup, dist, use_graph=not args.no_graph)
+        c1 = {"us": r1["launch_ms_mean"] * 1e3, "parity": parity_check("hdiff", "f64", r1["sets"])}
+        if not args.no_cpu_baseline:
+            t1 = time_reference("hdiff", "f64", dom1, seconds=3.0, max_calls=2000)
+            if t1:
+                c1["cpu_ref_us"] = statistics.median(t1) * 1e6
+        extra["c1"] = c1
+        dy = _extra_guard(dycore_timed, dist)
+        if "achieved_gbs" in dy:
+            dy["frac"] = dy.pop("achieved_gbs") / peak
+        extra["dycore"] = dy
+        extra["dycore_fused_peer"] = _extra_guard(dycore_fused_peer, dist)
+    if dist.world > 1 and not args.no_extra:
+        extra["dycore_decomposed_peer"] = _extra_guard(dycore_decomposed_peer, dist)
+        extra["dycore_fused_peer"] = _extra_guard(dycore_fused_peer, dist)
+    if extra and dist.rank == 0:
+        detail["extra"] = extra
+        line["extra"] = {k: {kk: vv for kk, vv in v.items() if kk not in ("workload", "unit", "value")}
+                         if isinstance(v, dict) else v for k, v in extra.items()}
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
         cores, model = host_info()
         times = time_reference(kernel, dtype, domain, seconds=args.cpu_seconds, max_calls=100000)
         if times:
             v = pts / statistics.median(times)
+            rows = cpu_rows(kernel, dtype, domain, cores)
+            detail["cpu_rows"] = rows
             line["cpu_baseline"] = {
                 "value": v, "unit": "grid-points/s", "cores": cores, "kind": "reference",
-                "sample": f"{len(times)} full {domain[0]}x{domain[1]}x{domain[2]} calls (median) of the "
-                          f"reference gen engine's own generated C kernel (oracle/_ref), OpenMP over "
-                          f"{cores} host threads ({model}), ~{args.cpu_seconds:.0f} s",
-                "min_call_ms": min(times) * 1e3, "median_call_ms": statistics.median(times) * 1e3,
+                "sample": f"median of {len(times)} full-domain calls, reference gen kernel (oracle/_ref)",
+                "rows": {k: _r(vv.get("value")) if isinstance(vv, dict) else vv for k, vv in rows.items()},
             }
-            line["cpu_baseline"]["rows"] = cpu_rows(kernel, dtype, domain, cores)
     done.set()
     if dist.rank == 0:
-        print(json.dumps(line), flush=True)
+        detail["line"] = line
+        try:
+            _detail_path(dist).write_text(json.dumps(detail, indent=1, default=str))
+        except OSError:
+            pass
+        print(json.dumps(_r(line)), flush=True)
 
 
 def main():

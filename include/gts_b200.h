@@ -11,7 +11,7 @@
  *
  *  2. One generated module per compiled stencil
  *     (<cache>/<fingerprint>/module.so), exporting GTS_B200_ENTRY below plus
- *     the three gts_b200_module_* functions.
+ *     the four gts_b200_module_* functions.
  *
  * All functions return 0 on success, otherwise a cudaError_t value or one of
  * the GTS_B200_ERR_* codes; gts_b200_error_string() renders either.
@@ -57,6 +57,9 @@ typedef int (*gts_b200_entry_fn)(int64_t ni, int64_t nj, int64_t nk, ...);
 int gts_b200_module_set_device(int device);
 int gts_b200_module_abi(void);
 int gts_b200_module_release(void); /* frees the module's temporary arenas */
+/* Kernels the module's entry has enqueued since load (fallback and helper
+ * kernels included): the launch count bench.py reports. */
+unsigned long long gts_b200_module_launch_count(void);
 
 /* ------------------------------------------------------------------------
  * libgts_b200.so: runtime services.
@@ -76,6 +79,10 @@ int gts_b200_malloc(void** ptr, size_t bytes);
 int gts_b200_free(void* ptr);
 int gts_b200_host_alloc(void** ptr, size_t bytes); /* pinned host memory */
 int gts_b200_host_free(void* ptr);
+/* page-lock / release an existing host buffer in place (mirror mode on the
+ * reference's pageable storages); *registered = 0 if it was already pinned */
+int gts_b200_host_register(void* ptr, size_t bytes, int* registered);
+int gts_b200_host_unregister(void* ptr);
 int gts_b200_memset(void* dst, int value, size_t bytes, void* stream);
 int gts_b200_memcpy_h2d(void* dst, const void* src, size_t bytes, void* stream);
 int gts_b200_memcpy_d2h(void* dst, const void* src, size_t bytes, void* stream);

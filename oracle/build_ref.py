@@ -1,4 +1,5 @@
-"""Build oracle/_ref: the REFERENCE's own native kernels for hdiff / vadv.
+"""Build oracle/_ref: the REFERENCE's own native kernels for hdiff / vadv
+(and the dycore step).
 
 TEST / BASELINE INFRASTRUCTURE ONLY (never linked by the product).
 
@@ -33,7 +34,13 @@ KERNELS = {
     "hdiff_f32": ("hdiff", "f32"),
     "vadv_f64": ("vadv", None),
     "vadv_f32": ("vadv", "f32"),
+    # BASELINE configs[4]: the dycore step, authored in the reference DSL
+    # (paper_2311_08322_b200/kernels/dycore.gts; the reference ships no
+    # dycore) and compiled by the reference's own gen emitter -- the
+    # full-size multi-step parity checker
+    "dycore_f64": ("dycore", None),
 }
+DYCORE_GTS = HERE.parent / "paper_2311_08322_b200" / "kernels" / "dycore.gts"
 
 
 def main() -> int:
@@ -52,7 +59,7 @@ def main() -> int:
     env = dict(os.environ)
     env.pop("CC", None)
     for key, (name, dt) in KERNELS.items():
-        src = kernel_source(name)
+        src = DYCORE_GTS.read_text() if name == "dycore" else kernel_source(name)
         if dt:
             src = src.replace("Field[f64]", f"Field[{dt}]")
         items = inline_functions(parse_program(src))

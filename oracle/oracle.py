@@ -15,6 +15,12 @@ Two independent restatements of the reference algorithms live here:
   and ``kernels/vadv.gts:4-16`` in the association order of the lowered IR
   (``pkg/tests/golden/hdiff_implementation.txt:11-24``).
 
+A third route runs the REFERENCE's own native kernels: ``oracle/_ref`` (built
+by ``build_ref.py`` from the reference's gen emitter, ``gen.py:229-369``)
+holds hdiff / vadv (f64, f32) and the dycore step; ``ref_*`` below call them
+on logical arrays (gen ABI, ``gen.py:5-14``).  They are the full-size checker
+of bench.py and of the GPU tests.
+
 Pinning: ``tests/test_oracle.py`` checks both restatements bitwise against
 the golden vectors in ``tests/golden/`` that ``tests/golden/make_golden.py``
 produced by running the reference's own ``vec`` and ``debug`` backends.
@@ -194,6 +200,94 @@ def vadv_np(a, b, c, d) -> np.ndarray:
         x[:, :, k] = dp[:, :, k].astype(np.float64) - (
             cp[:, :, k].astype(np.float64) * x[:, :, k + 1].astype(np.float64))
     return x
+
+
+# ---------------------------------------------------------------------------
+# The reference's own generated kernels (oracle/_ref)
+# ---------------------------------------------------------------------------
+
+REF_DIR = HERE / "_ref"
+_ref_fns: dict = {}
+
+
+def ref_manifest() -> dict:
+    p = REF_DIR / "manifest.json"
+    if not p.exists():
+        return {}
+    import json
+
+    return json.loads(p.read_text())
+
+
+def ref_available(key: str) -> bool:
+    man = ref_manifest().get(key)
+    return man is not None and (REF_DIR / man["so"]).exists()
+
+
+def _ref_fn(key: str):
+    if key not in _ref_fns:
+        man = ref_manifest()[key]
+        lib = ctypes.CDLL(str(REF_DIR / man["so"]))
+        fn = getattr(lib, man["symbol"])
+        nf = len(man["fields"])
+        fn.argtypes = [ctypes.c_longlong] * 3 + ([ctypes.c_void_p] + [ctypes.c_longlong] * 6) * nf + \
+            [ctypes.c_float if d == "f32" else ctypes.c_double for _, d in man["scalars"]]
+        fn.restype = None
+        _ref_fns[key] = (fn, man)
+    return _ref_fns[key]
+
+
+def gen_layout(arr: np.ndarray) -> np.ndarray:
+    """Copy of a logical (i, j, k) array laid out k-outermost, j-contiguous
+    (the gen layout, storage.py:60-64), returned as a logical view."""
+    g = np.empty((arr.shape[2], arr.shape[0], arr.shape[1]), dtype=arr.dtype)
+    g[...] = arr.transpose(2, 0, 1)
+    return g.transpose(1, 2, 0)
+
+
+def ref_call(key: str, domain, fields: dict, scalars: dict) -> None:
+    """Run the reference kernel ``key`` over ``domain`` on logical arrays
+    ``fields`` = {name: (array, origin)} (written in place)."""
+    fn, man = _ref_fn(key)
+    args = [int(domain[0]), int(domain[1]), int(domain[2])]
+    for n in man["fields"]:
+        arr, org = fields[n]
+        args += _field_args(arr, org)
+    for n, _ in man["scalars"]:
+        args.append(float(scalars[n]))
+    fn(*args)
+
+
+def ref_hdiff(inp: np.ndarray, coeff: float) -> np.ndarray:
+    """The reference gen engine's hdiff on a (ni+4, nj+4, nk) block."""
+    key = "hdiff_" + _sfx(inp.dtype)
+    dom = (inp.shape[0] - 4, inp.shape[1] - 4, inp.shape[2])
+    out = gen_layout(np.zeros(dom, dtype=inp.dtype))
+    ref_call(key, dom, {"inp": (gen_layout(inp), (2, 2, 0)), "out": (out, (0, 0, 0))}, {"coeff": coeff})
+    return np.ascontiguousarray(out)
+
+
+def ref_vadv(a, b, c, d) -> np.ndarray:
+    key = "vadv_" + _sfx(a.dtype)
+    x = gen_layout(np.zeros(a.shape, dtype=a.dtype))
+    f = {n: (gen_layout(v), (0, 0, 0)) for n, v in zip("abcd", (a, b, c, d))}
+    f["x"] = (x, (0, 0, 0))
+    ref_call(key, a.shape, f, {})
+    return np.ascontiguousarray(x)
+
+
+def ref_dycore_run(u: np.ndarray, a, b, c, steps: int, coeff: float = 0.05, tau: float = 0.2) -> np.ndarray:
+    """``steps`` dycore steps by the reference gen engine's own kernel for
+    kernels/dycore.gts, with the host swap of u_in / u_out (the 2-cell halo
+    keeps its initial values); returns the final u with its halo."""
+    dom = (u.shape[0] - 4, u.shape[1] - 4, u.shape[2])
+    bufs = [gen_layout(u), gen_layout(u)]
+    coef = {n: (gen_layout(v), (0, 0, 0)) for n, v in zip("abc", (a, b, c))}
+    for s in range(steps):
+        src, dst = bufs[s % 2], bufs[(s + 1) % 2]
+        ref_call("dycore_f64", dom, {"u_in": (src, (2, 2, 0)), "u_out": (dst, (2, 2, 0)), **coef},
+                 {"coeff": coeff, "tau": tau})
+    return np.ascontiguousarray(bufs[steps % 2])
 
 
 def max_rel(a: np.ndarray, b: np.ndarray) -> float:

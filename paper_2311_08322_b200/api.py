@@ -32,28 +32,22 @@ _reference_compile = sf_runtime.compile_stencil
 
 
 def _select_definition(source: str, stencil_name: Optional[str], externals: dict, file):
-    """The frontend half of runtime.compile_stencil (runtime.py:278-303)."""
-    from stencilforge.frontend import bind_externals, inline_functions, parse_program
+    """Parse, inline and bind through the reference's own frontend
+    (``runtime.frontend_pipeline``, runtime.py:326-341), after the one rule
+    ``compile_stencil`` adds to it: a program with several stencils needs
+    ``stencil_name`` (runtime.py:283-291)."""
+    if stencil_name is None:
+        from stencilforge.frontend import inline_functions, parse_program
 
-    try:
-        items = parse_program(source, file)
-        stencils = inline_functions(items)
-        if not stencils:
-            raise DslError(Code.SYNTAX, ir.UNKNOWN_SPAN, "no stencil in program")
-        if stencil_name is None:
-            if len(stencils) > 1:
-                names = ", ".join(s.name for s in stencils)
-                raise DslError(Code.SYNTAX, ir.UNKNOWN_SPAN,
-                               f"program has multiple stencils ({names}); pass stencil_name")
-            definition = stencils[0]
-        else:
-            match = [s for s in stencils if s.name == stencil_name]
-            if not match:
-                raise DslError(Code.SYNTAX, ir.UNKNOWN_SPAN, f"no stencil named '{stencil_name}'")
-            definition = match[0]
-        return bind_externals(definition, externals)
-    except DslError as exc:
-        raise CompilationError([exc.as_diagnostic()])
+        try:
+            names = [s.name for s in inline_functions(parse_program(source, file))]
+        except DslError as exc:
+            raise CompilationError([exc.as_diagnostic()])
+        if len(names) > 1:
+            err = DslError(Code.SYNTAX, ir.UNKNOWN_SPAN,
+                           f"program has multiple stencils ({', '.join(names)}); pass stencil_name")
+            raise CompilationError([err.as_diagnostic()])
+    return sf_runtime.frontend_pipeline(source, stencil_name, externals, file)
 
 
 @dataclass(frozen=True)
@@ -84,13 +78,11 @@ class B200CompiledStencil(sf_runtime.CompiledStencil):
     time_device: bool = False
 
     def __call__(self, *, domain=None, origin=None, validate=None, **arguments):
-        prev = b200_backend.TIME_DEVICE
-        b200_backend.TIME_DEVICE = prev or self.time_device
-        try:
+        # per-thread timing flag and per-thread call statistics: concurrent
+        # calls from other threads neither see nor change them
+        with b200_backend.device_timing(self.time_device):
             rep = super().__call__(domain=domain, origin=origin, validate=validate, **arguments)
-        finally:
-            b200_backend.TIME_DEVICE = prev
-        t = b200_backend.last_transfer
+        t = b200_backend.call_stats()
         return B200ExecutionReport(rep.total_ns, rep.validate_ns, rep.kernel_ns, rep.domain, rep.validated,
                                    t.get("device_ns"), t.get("kernel_device_ns"), int(t.get("h2d", 0)),
                                    int(t.get("d2h", 0)))

@@ -20,12 +20,13 @@ from __future__ import annotations
 
 import ctypes
 import os
+import threading
 import weakref
 from typing import Optional
 
 from . import native
 from ._host import BackendError, Code, ir, sf_common
-from .codegen import entry_name, generate_source, mirror_setter_name
+from .codegen import entry_name, frame_setter_name, generate_source, mirror_setter_name
 from .lowering import build_plan
 from .storage import DeviceFieldStorage, FieldStorage
 from .toolchain import BuildCache, load_library
@@ -33,8 +34,39 @@ from .toolchain import BuildCache, load_library
 BACKEND_ID = "b200"
 
 
+# host buffers page-locked in place by the mirror mode: id(numpy base) ->
+# registration (unregistered when the buffer is garbage collected)
+_pinned_in_place: dict = {}
+_pin_lock = threading.Lock()
+# the reference's own storages are pageable numpy memory (stencilforge
+# storage.py:130-160); pinning them in place on first use turns their copies
+# from the driver's staged pageable path into full-speed DMA
+PIN_HOST = os.environ.get("GTS_B200_PIN_HOST", "1") != "0"
+
+
+def _pin_host_buffer(base) -> None:
+    key = id(base)
+    with _pin_lock:
+        if key in _pinned_in_place:
+            return
+        reg = ctypes.c_int(0)
+        st = native.lib().gts_b200_host_register(base.ctypes.data, base.nbytes, ctypes.byref(reg))
+        _pinned_in_place[key] = bool(reg.value) if st == 0 else False
+        if st == 0 and reg.value:
+            weakref.finalize(base, _unpin_host_buffer, key, base.ctypes.data)
+
+
+def _unpin_host_buffer(key, ptr) -> None:  # pragma: no cover - GC path
+    _pinned_in_place.pop(key, None)
+    try:
+        native.lib().gts_b200_host_unregister(ptr)
+    except Exception:
+        pass
+
+
 class _Mirror:
-    """Cached device twin of a host FieldStorage (mirror mode)."""
+    """Cached device twin of a host FieldStorage (mirror mode).  A pageable
+    host buffer is page-locked in place once (``PIN_HOST``)."""
 
     def __init__(self, storage: FieldStorage):
         self.nbytes = storage._base.nbytes
@@ -43,6 +75,8 @@ class _Mirror:
         self.dptr = p.value
         self.host_base = storage._base.ctypes.data
         self._fin = weakref.finalize(self, _Mirror._release, self.dptr)
+        if PIN_HOST:
+            _pin_host_buffer(storage._base)
 
     @staticmethod
     def _release(dptr):  # pragma: no cover - GC path
@@ -55,11 +89,14 @@ class _Mirror:
         return self.dptr + (storage.base_address() - self.host_base)
 
 
+# device twins of host storages, per (stream, host buffer): a thread's calls
+# (one stream per thread, native.default_stream) never share a twin with
+# another thread's concurrent call
 _mirrors: dict = {}
 
 
-def _mirror_for(storage: FieldStorage) -> _Mirror:
-    key = id(storage._base)
+def _mirror_for(storage: FieldStorage, stream: int) -> _Mirror:
+    key = (stream, id(storage._base))
     m = _mirrors.get(key)
     if m is None or m.host_base != storage._base.ctypes.data or m.nbytes != storage._base.nbytes:
         m = _Mirror(storage)
@@ -92,6 +129,8 @@ class Module:
         self.fn = fn
         self.lib.gts_b200_module_set_device.argtypes = [ctypes.c_int]
         self.lib.gts_b200_module_set_device.restype = ctypes.c_int
+        self.lib.gts_b200_module_launch_count.argtypes = []
+        self.lib.gts_b200_module_launch_count.restype = ctypes.c_ulonglong
         self._device = None
         self.field_order = [f.name for f in impl.api_fields]
         self.scalar_order = [s.name for s in impl.api_scalars]
@@ -102,9 +141,28 @@ class Module:
             self._mirror_fn.restype = ctypes.c_int
         except AttributeError:
             self._mirror_fn = None
+        try:  # present for single fused PARALLEL kernels (codegen frame_ok)
+            self._frame_fn = getattr(self.lib, frame_setter_name(impl, fp))
+            self._frame_fn.argtypes = [ctypes.c_int, ctypes.c_int]
+            self._frame_fn.restype = ctypes.c_int
+        except AttributeError:
+            self._frame_fn = None
+
+    @property
+    def frame_supported(self) -> bool:
+        """The module can run a decomposed step's boundary as ONE frame launch
+        (only the tiles touching the halo-dependent band; idempotent
+        recomputation of band-adjacent interior points)."""
+        return self._frame_fn is not None
+
+    def launch_count(self) -> int:
+        """Kernels this module has enqueued so far (every launch its entry
+        made, fallback and helper kernels included)."""
+        return int(self.lib.gts_b200_module_launch_count())
 
     def set_mirror(self, boxes) -> None:
-        """Halo-mirror boxes for the next launches (gen_options ``mirror``):
+        """Halo-mirror boxes for the calling thread's NEXT launch of this
+        module, consumed by it (gen_options ``mirror``):
         ``boxes`` = [(i0, i1, j0, j1, base_address, s_i, s_j, s_k)], at most 8,
         in the launch's domain coordinates; element (i, j, k) of a box is also
         stored at base + (i*s_i + j*s_j + k*s_k) * itemsize."""
@@ -132,6 +190,7 @@ class Module:
             if not isinstance(st, DeviceFieldStorage):
                 raise TypeError(f"launcher needs device-resident fields; '{name}' is {type(st).__name__}")
             st.to_device(stream)
+            st.wait_producer(stream)
             args.append(st.base_address())
             args.extend(int(s) for s in st.strides)
             args.extend(int(o) + int(d) for o, d in zip(st.origin, offset))
@@ -140,15 +199,37 @@ class Module:
         args.append(stream)
         fn, sym = self.fn, self.symbol
         written = [fields[n] for n in self.written]
+        bound = list({id(st): st for st in fields.values()}.values())
 
         def go() -> None:
+            # host writes made through .view since the launcher was built land
+            # first, so marking the outputs device-written loses nothing
+            for st in bound:
+                if st._host_dirty:
+                    st.to_device(stream)
             status = fn(*args)
             if status:
                 raise native.DeviceError(status, sym)
             for w in written:
-                w._device_dirty = True
+                w.mark_device_written(stream)
 
         return go
+
+    def frame_launcher(self, domain, fields: dict, scalars: dict, stream: int, band) -> callable:
+        """Like ``launcher`` over the whole domain, but every enqueue first
+        requests a frame launch for the calling thread: only the tiles with a
+        point inside the band of width ``band`` = (hi, hj) along the domain's
+        sides run (the rest is the interior launch's)."""
+        if self._frame_fn is None:
+            raise BackendError(Code.COMPILE_FAILED, f"{self.symbol}: no frame launch for this plan")
+        go = self.launcher(domain, fields, scalars, stream)
+        fr, hi, hj = self._frame_fn, int(band[0]), int(band[1])
+
+        def go_frame() -> None:
+            native.check(fr(hi, hj), "frame request")
+            go()
+
+        return go_frame
 
     def launch(self, domain, pointers: dict, strides: dict, origins: dict, scalars: dict,
                stream: int) -> None:
@@ -167,26 +248,62 @@ class Module:
             raise native.DeviceError(status, f"{self.symbol}")
 
 
-# bytes moved by the last mirror-mode call (bench.py's e2e line reports them)
-# what the last run() moved and how long the device took (B200ExecutionReport):
-# device_ns = first host->device copy .. last device->host copy (or the launch
-# alone for device storages), kernel_ns = the stencil launches only (None when
-# they interleave with copies in the pipelined mirror mode)
-last_transfer: dict = {"h2d": 0, "d2h": 0, "chunks": 0, "device_ns": None, "kernel_device_ns": None}
+# Per-call state lives in thread-local storage, never in module globals, so
+# concurrent calls from several threads do not see each other's:
+# ``call_stats()`` = what the calling thread's last run() moved and how long
+# the device took (B200ExecutionReport): device_ns = first host->device copy ..
+# last device->host copy (or the launch alone for device storages),
+# kernel_device_ns = the stencil launches only (None when they interleave with
+# copies in the pipelined mirror mode).
+_tls = threading.local()
+
+
+def call_stats() -> dict:
+    st = getattr(_tls, "stats", None)
+    if st is None:
+        st = _tls.stats = {"h2d": 0, "d2h": 0, "chunks": 0, "device_ns": None, "kernel_device_ns": None}
+    return st
+
+
 # CUDA-event device timing of run() (4 event records + 2 queries, ~20 us per
-# call from Python, so opt-in: B200CompiledStencil.time_device or the
-# GTS_B200_DEVICE_TIME=1 environment variable)
+# call from Python, so opt-in: B200CompiledStencil.time_device for its own
+# calls, or GTS_B200_DEVICE_TIME=1 for every call)
 TIME_DEVICE = os.environ.get("GTS_B200_DEVICE_TIME") == "1"
-_events: list = []
+
+
+def time_device() -> bool:
+    return TIME_DEVICE or getattr(_tls, "time_device", False)
+
+
+class device_timing:
+    """``with device_timing(on):`` -- CUDA-event timing of the calling
+    thread's run() calls inside the block (no global state is touched)."""
+
+    def __init__(self, on: bool = True):
+        self.on = on
+
+    def __enter__(self):
+        self.prev = getattr(_tls, "time_device", False)
+        _tls.time_device = self.prev or self.on
+        return self
+
+    def __exit__(self, *a):
+        _tls.time_device = self.prev
+        return False
 
 
 PIPE_TRACE = None  # a list to collect per-call device spans of the pipelined mirror mode (probes)
 
 
 def _event(i: int):
-    while len(_events) <= i:
-        _events.append(native.Event())
-    return _events[i]
+    """The calling thread's event slot ``i``."""
+    evs = getattr(_tls, "events", None)
+    if evs is None:
+        evs = _tls.events = {}
+    ev = evs.get(i)
+    if ev is None:
+        ev = evs[i] = native.Event()
+    return ev
 
 
 def _interval_range(iv, nk: int) -> tuple:
@@ -318,13 +435,13 @@ class _Pipeline:
         ni, nj, nk = domain
         comp = native.default_stream()
         up, down = native.aux_stream("h2d"), native.aux_stream("d2h")
-        timed = TIME_DEVICE or PIPE_TRACE is not None
+        timed = time_device() or PIPE_TRACE is not None
         if timed:
             _event(1000).record(up)
         mirrors, ptrs, strides, origins = {}, {}, {}, {}
         for n in self.module.field_order:
             st, org = field_args[n]
-            m = _mirror_for(st)
+            m = _mirror_for(st, comp)
             mirrors[n] = m
             ptrs[n] = m.device_address(st)
             strides[n] = tuple(int(x) for x in st.strides)
@@ -384,11 +501,12 @@ class _Pipeline:
             _event(1003).record(down)
         native.synchronize(down)
         native.synchronize(comp)
-        last_transfer.update(h2d=h2d, d2h=d2h, chunks=nch)
+        stats = call_stats()
+        stats.update(h2d=h2d, d2h=d2h, chunks=nch)
         if timed:
             t0 = _event(1000)
             span = max(t0.elapsed_ms(_event(1002)), t0.elapsed_ms(_event(1003)))
-            last_transfer.update(device_ns=int(span * 1e6))
+            stats.update(device_ns=int(span * 1e6))
         if PIPE_TRACE is not None:
             t0 = _event(1000)
             PIPE_TRACE.append({"h2d_ms": t0.elapsed_ms(_event(1001)), "kernels_ms": t0.elapsed_ms(_event(1002)),
@@ -426,12 +544,13 @@ def build(impl, fp, cache: Optional[BuildCache] = None, options: Optional[dict] 
         for name in module.field_order:
             storage, origin = field_args[name]
             if isinstance(storage, DeviceFieldStorage):
-                storage.to_device(stream, sync=False)
+                storage.to_device(stream)
+                storage.wait_producer(stream)
                 pointers[name] = storage.base_address()
             else:
                 key = id(storage._base)
                 if key not in mirrors:
-                    m = _mirror_for(storage)
+                    m = _mirror_for(storage, stream)
                     native.call("gts_b200_memcpy_h2d", m.dptr, m.host_base, m.nbytes, stream)
                     mirrors[key] = (m, storage)
                 pointers[name] = mirrors[key][0].device_address(storage)
@@ -451,10 +570,11 @@ def build(impl, fp, cache: Optional[BuildCache] = None, options: Optional[dict] 
         if not all(type(st) is DeviceFieldStorage for st in sts):
             return False
         module.bind_device()
-        key = (module._device, tuple(domain),
-               tuple((id(st), st.base_address(), tuple(field_args[n][1])) for n, st in zip(order, sts)),
-               tuple(float(scalar_args[n]) for n in sorder))
         stream = native.default_stream()
+        key = (module._device, stream, tuple(domain),
+               tuple((id(st), st.base_address(), tuple(st.strides), tuple(st.shape), tuple(field_args[n][1]))
+                     for n, st in zip(order, sts)),
+               tuple(float(scalar_args[n]) for n in sorder))
         args = fast.get(key)
         if args is None:
             args = [int(domain[0]), int(domain[1]), int(domain[2])]
@@ -469,26 +589,27 @@ def build(impl, fp, cache: Optional[BuildCache] = None, options: Optional[dict] 
             fast[key] = args
         for st in sts:
             if st._host_dirty:
-                st.to_device(stream, sync=False)
+                st.to_device(stream)
         status = module.fn(*args)
         if status:
             raise native.DeviceError(status, module.symbol)
-        for n in written:
-            field_args[n][0]._device_dirty = True
         native.synchronize(stream)
+        for n in written:
+            field_args[n][0].mark_device_written()
         return True
 
     def run(domain, field_args, scalar_args) -> None:
-        last_transfer.update(h2d=0, d2h=0, chunks=0, device_ns=None, kernel_device_ns=None)
+        stats = call_stats()
+        stats.update(h2d=0, d2h=0, chunks=0, device_ns=None, kernel_device_ns=None)
         if any(d == 0 for d in domain):
             return
-        if not TIME_DEVICE and run_device(domain, field_args, scalar_args):
+        timed = time_device()
+        if not timed and run_device(domain, field_args, scalar_args):
             return
         if pipe.eligible(domain, field_args):
             pipe.run(domain, field_args, scalar_args)
             return
         stream = native.default_stream()
-        timed = TIME_DEVICE
         if timed:
             _event(2000).record(stream)
         pointers, strides, origins, mirrors = prepare(field_args, stream)
@@ -497,12 +618,12 @@ def build(impl, fp, cache: Optional[BuildCache] = None, options: Optional[dict] 
         module.launch(domain, pointers, strides, origins, scalar_args, stream)
         if timed:
             _event(2002).record(stream)
-        last_transfer.update(h2d=sum(m.nbytes for m, _ in mirrors.values()), d2h=0, chunks=0)
+        stats.update(h2d=sum(m.nbytes for m, _ in mirrors.values()), d2h=0, chunks=0)
         copied = set()
         for name in module.written:
             storage, _ = field_args[name]
             if isinstance(storage, DeviceFieldStorage):
-                storage.mark_device_written()
+                storage.mark_device_written()  # the stream is synchronised below
             else:
                 key = id(storage._base)
                 if key in copied:
@@ -510,13 +631,13 @@ def build(impl, fp, cache: Optional[BuildCache] = None, options: Optional[dict] 
                 copied.add(key)
                 m = mirrors[key][0]
                 native.call("gts_b200_memcpy_d2h", m.host_base, m.dptr, m.nbytes, stream)
-                last_transfer["d2h"] += m.nbytes
+                stats["d2h"] += m.nbytes
         if timed:
             _event(2003).record(stream)
         native.synchronize(stream)
         if timed:
-            last_transfer.update(device_ns=int(_event(2000).elapsed_ms(_event(2003)) * 1e6),
-                                 kernel_device_ns=int(_event(2001).elapsed_ms(_event(2002)) * 1e6))
+            stats.update(device_ns=int(_event(2000).elapsed_ms(_event(2003)) * 1e6),
+                         kernel_device_ns=int(_event(2001).elapsed_ms(_event(2002)) * 1e6))
 
     build_info = {
         "cache_hit": cache_hit,

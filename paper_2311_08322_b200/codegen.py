@@ -26,6 +26,7 @@ exact hex literals (``gen.py:111-116``).
 from __future__ import annotations
 
 import math
+import re
 import threading
 from typing import Optional
 
@@ -471,6 +472,22 @@ def generate_source(plan: Plan, fp, options: Optional[dict] = None) -> str:
         return _generate_source(plan, fp, options)
 
 
+def frame_setter_name(impl, fp) -> str:
+    """Exported request for a frame launch (decomp.DecomposedStep): the
+    calling thread's next launch computes only the tiles that touch the band
+    of width (hi, hj) along the domain's sides."""
+    return "gts_frame_" + entry_name(impl, fp)[len("gts_run_"):]
+
+
+def written_api_fields(impl) -> list:
+    api = [f.name for f in impl.api_fields]
+    w = set()
+    for ms in impl.multistages:
+        for st in ms.stages:
+            w |= writes(st.body)
+    return [n for n in api if n in w]
+
+
 def mirror_setter_name(impl, fp) -> str:
     """Exported setter of the halo-mirror boxes (gen_options ``mirror``)."""
     return "gts_mirror_" + entry_name(impl, fp)[len("gts_run_"):]
@@ -495,7 +512,7 @@ def _mirror_field(plan: Plan, opts: dict):
 
 def _generate_source(plan: Plan, fp, options: Optional[dict] = None) -> str:
     impl = plan.impl
-    from . import codegen_column, codegen_parallel, codegen_rowstream  # template instantiations
+    from . import codegen_column, codegen_parallel  # template instantiations
 
     opts = options or {}
 
@@ -537,10 +554,11 @@ def _generate_source(plan: Plan, fp, options: Optional[dict] = None) -> str:
     w("};")
     w("")
     if mirror:
-        # host-side mirror boxes, set by gts_mirror_<name>_<digest8> and copied
-        # into every launch's parameters (so a CUDA graph captures the boxes
-        # that were set when the launch was captured)
-        w(f"static GtsMirror<{ctype[mirror]}> g_mirror;")
+        # host-side mirror boxes, set by gts_mirror_<name>_<digest8> for the
+        # calling thread's NEXT launch and consumed by it (copied into that
+        # launch's parameters, so a CUDA graph captures the boxes set for the
+        # captured launch; no box outlives the launch it was set for)
+        w(f"static thread_local GtsMirror<{ctype[mirror]}> g_mirror;")
         w('extern "C" __attribute__((visibility("default")))')
         w(f"int {mirror_setter_name(impl, fp)}(int n, const int64_t* desc) {{")
         w(f"  if (n < 0 || n > 8) return {GTS_ERR_UNSUPPORTED};")
@@ -551,6 +569,23 @@ def _generate_source(plan: Plan, fp, options: Optional[dict] = None) -> str:
         w(f"    g_mirror.base[d] = ({ctype[mirror]}*)(intptr_t)q[4];")
         w("    g_mirror.si[d] = q[5]; g_mirror.sj[d] = q[6]; g_mirror.sk[d] = q[7];")
         w("  }")
+        w("  return 0;")
+        w("}")
+        w("")
+
+    # frame launches (decomp.DecomposedStep): a single fused PARALLEL kernel
+    # whose re-execution on a point is idempotent (no api field both read and
+    # written), so frame tiles may recompute points the interior launch wrote
+    api_reads = {a.field for ms in impl.multistages for st in ms.stages for a in reads(st.body)}
+    api_written = set(written_api_fields(impl))
+    frame_ok = (len(plan.kernels) == 1 and plan.kernels[0].kind == "pfused"
+                and not (api_reads & api_written) and opts.get("pf_frame_variant", True))
+    if frame_ok:
+        w("static thread_local int g_frame_hi = -1, g_frame_hj = -1;")
+        w('extern "C" __attribute__((visibility("default")))')
+        w(f"int {frame_setter_name(impl, fp)}(int hi, int hj) {{")
+        w("  if (hi < 0 || hj < 0) return %d;" % GTS_ERR_UNSUPPORTED)
+        w("  g_frame_hi = hi; g_frame_hj = hj;  // the calling thread's NEXT launch only")
         w("  return 0;")
         w("}")
         w("")
@@ -600,20 +635,21 @@ def _generate_source(plan: Plan, fp, options: Optional[dict] = None) -> str:
             saved_launches = launches
             if fused_col is not None:
                 launches = []
-            res = resL = resT = None
+            res = resL = resT = resF = None
             if opts.get("tma", True):
-                if opts.get("pf_mode", "tile") == "row":
-                    res = codegen_rowstream.emit(kname, plan, k, ctype, dtypes, opts)
-                else:
-                    res = codegen_parallel.emit(kname, plan, k, ctype, dtypes, opts)
-                    # binary64 groups: extra geometries for large and for tiny domains,
-                    # chosen at launch (codegen_parallel.LARGE / TINY)
-                    if (res is not None and codegen_parallel.last_esize() == 8 and "pf_nw" not in opts
-                            and "pf_ri" not in opts and opts.get("pf_dual", True)):
-                        resL = codegen_parallel.emit(kname + "L", plan, k, ctype, dtypes,
-                                                     {**opts, **codegen_parallel.LARGE})
-                        resT = codegen_parallel.emit(kname + "T", plan, k, ctype, dtypes,
-                                                     {**opts, **codegen_parallel.TINY})
+                res = codegen_parallel.emit(kname, plan, k, ctype, dtypes, opts)
+                # binary64 groups: extra geometries for large and for tiny domains,
+                # chosen at launch (codegen_parallel.LARGE / TINY)
+                if (res is not None and codegen_parallel.last_esize() == 8 and "pf_nw" not in opts
+                        and "pf_ri" not in opts and opts.get("pf_dual", True)):
+                    resL = codegen_parallel.emit(kname + "L", plan, k, ctype, dtypes,
+                                                 {**opts, **codegen_parallel.LARGE})
+                    resT = codegen_parallel.emit(kname + "T", plan, k, ctype, dtypes,
+                                                 {**opts, **codegen_parallel.TINY})
+                # the frame launch of a decomposed step (decomp.DecomposedStep)
+                if res is not None and frame_ok:
+                    resF = codegen_parallel.emit(kname + "F", plan, k, ctype, dtypes,
+                                                 {**opts, **codegen_parallel.FRAME_GEOMETRY})
             fb = []
             for r in k.stages:
                 nm = f"{kname}_s{r.idx}"
@@ -652,6 +688,22 @@ def _generate_source(plan: Plan, fp, options: Optional[dict] = None) -> str:
                     fused_ok[kidx] = f"({flag} || {flagL})"
                 launches += (head + [f"  if ({flag} && (fzs_{kidx} || !{flagL})) {{"] + launch
                              + [f"  }} else if ({flagL}) {{"] + launchL + ["  } else {"] + fb + ["  }"])
+            if resF is not None:
+                # frame requested (gts_frame_<name>_<digest8>) and the frame
+                # variant's tensor maps are valid: the frame tiles only;
+                # otherwise the full launch below (idempotent: frame_ok)
+                codeF, preF, launchF = resF
+                out.extend(codeF)
+                flagF = f"fz_okF_{kidx}"
+                prelude += [ln.replace(f"fz_ok_{kidx}", flagF) for ln in preF]
+                pos = len(launches) - 1
+                while not launches[pos].startswith("  if ("):
+                    pos -= 1
+                while pos > 0 and launches[pos - 1] == "  } else":
+                    pos -= 1
+                    while not launches[pos].startswith("  if ("):
+                        pos -= 1
+                launches[pos:pos] = [f"  if (fr_hi >= 0 && {flagF}) {{"] + launchF + ["  } else"]
             if fused_col is not None:
                 pf_lines = launches
                 launches = saved_launches
@@ -761,8 +813,13 @@ def _generate_source(plan: Plan, fp, options: Optional[dict] = None) -> str:
         w(f"  p.f_{n} = gts_field(f_{n}, s_{n}_i, s_{n}_j, s_{n}_k, o_{n}_i, o_{n}_j, o_{n}_k);")
     for s in impl.api_scalars:
         w(f"  p.sc_{s.name} = sc_{s.name};")
+    if frame_ok:
+        w("  const int fr_hi = g_frame_hi, fr_hj = g_frame_hj;  // consumed by this launch")
+        w("  g_frame_hi = g_frame_hj = -1;")
     if mirror:
+        # the boxes apply to this launch only (set again before every launch)
         w("  p.mir = g_mirror;")
+        w("  g_mirror.n = 0;")
     out.extend(prelude)
     if arena_temps:
         w("  // device arena for temporaries: shape = domain + extent (common.py:58-69),")
@@ -777,7 +834,8 @@ def _generate_source(plan: Plan, fp, options: Optional[dict] = None) -> str:
             w(f"  const int64_t tp_{t} = gts_pad_row(td_{t}_j, sizeof({ctype[t]}));")
             w(f"  const size_t toff_{t} = arena_bytes;")
             w(f"  if (need_{t}) arena_bytes += gts_round_up((size_t)(td_{t}_i * tp_{t} * nk) * sizeof({ctype[t]}), 256);")
-        w("  char* arena = arena_bytes ? (char*)gts_arena(arena_bytes, st) : nullptr;")
+        w("  GtsArenaLease lease(arena_bytes, st);  // held until every launch below is enqueued")
+        w("  char* arena = lease.ptr;")
         w(f"  if (arena_bytes && !arena) return {GTS_ERR_ALLOC};")
         for t in arena_temps:
             e = temps[t].extent
@@ -795,4 +853,9 @@ def _generate_source(plan: Plan, fp, options: Optional[dict] = None) -> str:
     w("  return (int)cudaGetLastError();")
     w("}")
     w("")
-    return "\n".join(out)
+    # count every triple-chevron launch (gts_b200_module_launch_count; the
+    # gts_launch_pdl / gts_fill_nan helpers count their own)
+    return _LAUNCH_RE.sub(r"\1++g_gts_launches; \2", "\n".join(out))
+
+
+_LAUNCH_RE = re.compile(r"^([ \t]*)(\w+<<<)", re.M)

@@ -288,7 +288,9 @@ def _emit_point(stmt, ctx: _Ctx, ctype, api: set, out: list, indent: str, local:
 PREFETCH = 0  # gen_options pf_prefetch: stream rows loaded this many steps early
 SWZ = False  # gen_options pf_swz: lane-alternating paired row loads (bank spreading)
 PDL = "off"  # gen_options pf_pdl: programmatic dependent launch off | early | late
-DEFAULTS = {"pf_nw": 4, "pf_ri": 8, "pf_vj": 4, "pf_nbuf": 1, "pf_prefetch": 0, "pf_swz": 0, "pf_pdl": "off"}  # + pf_pdl: off|early|late
+FRAME = False  # frame variant: the launch enumerates only the tiles outside an inner tile rectangle
+DEFAULTS = {"pf_nw": 4, "pf_ri": 8, "pf_vj": 4, "pf_nbuf": 1, "pf_prefetch": 0, "pf_swz": 0, "pf_pdl": "off",
+            "pf_frame": 0}
 # Measured defaults per element size (profiles/sweep_hdiff_r1.md, hdiff
 # 256x256x80 on one B200, CUDA-graph timed):
 #  f64: 16x128 tiles, double-buffered TMA boxes: 16.9 us vs 18.1 us for
@@ -320,6 +322,11 @@ LARGE_POINTS = 16 * 1024 * 1024
 # but 192^2x80 12.54 -> 14.10 us (tools/abtest.py).
 TINY = {"pf_ri": 2}
 TINY_POINTS = 2 * 1024 * 1024
+# The frame launch of a decomposed step (decomp.DecomposedStep): after the
+# halo exchange, only the tiles that touch the halo-dependent band run, in
+# thin tiles (4 rows x 32 columns: 2 warps x 2 rows, 1 column per lane) so
+# the band's j-sides cost 2 x 32 columns instead of 2 x 128.
+FRAME_GEOMETRY = {"pf_ri": 2, "pf_vj": 1, "pf_frame": 1, "pf_swz": 0}
 _LAST_ESIZE = 0
 
 
@@ -333,13 +340,15 @@ def configure(opts, esize: int = 0) -> None:
     fingerprint like the reference gen engine's tile options, gen.py:235-238).
     Unset options take the measured default of the group's smallest streamed
     element size ``esize`` (0: the generic DEFAULTS)."""
-    global NW, RI, VJ, TJ, TI, NBUF, PREFETCH, SWZ, PDL
-    o = dict(GEOMETRY.get(esize, DEFAULTS))
+    global NW, RI, VJ, TJ, TI, NBUF, PREFETCH, SWZ, PDL, FRAME
+    o = dict(DEFAULTS)
+    o.update(GEOMETRY.get(esize, {}))
     o.update({k: v for k, v in (opts or {}).items() if k in DEFAULTS})
     NW, RI, VJ, NBUF = int(o["pf_nw"]), int(o["pf_ri"]), int(o["pf_vj"]), int(o["pf_nbuf"])
     PREFETCH = int(o["pf_prefetch"])
     SWZ = bool(int(o["pf_swz"]))
     PDL = str(o["pf_pdl"])
+    FRAME = bool(int(o["pf_frame"]))
     TJ, TI = 32 * VJ, NW * RI
 
 
@@ -373,8 +382,9 @@ def emit(kname: str, plan, kplan, ctype: dict, dtypes: dict, opts=None):
       f"{[(x.name, x.rlo, x.rhi, x.clo, x.chi) for x in regw]}")
     minb = int((opts or {}).get("pf_minb", 0))  # min resident CTAs/SM (register cap), 0 = compiler's choice
     lb = f"{32 * NW}, {minb}" if minb else f"{32 * NW}"
+    frame_args = ", int fi0, int fi1, int fj0, int fj1" if FRAME else ""
     w(f"__global__ void __launch_bounds__({lb}) {kname}(const __grid_constant__ GtsParams p, {tm}, "
-      "int k0, int nkr, int tiles_i, int tiles_j, int ntiles) {")
+      f"int k0, int nkr, int tiles_i, int tiles_j, int ntiles{frame_args}) {{")
     w("  extern __shared__ __align__(1024) unsigned char smem[];")
     w(f"  uint64_t* full = (uint64_t*)(smem + {bar_off});")
     w("  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;")
@@ -387,11 +397,23 @@ def emit(kname: str, plan, kplan, ctype: dict, dtypes: dict, opts=None):
         w("  gts_griddep_wait();  // PDL: previous grid complete before any global access")
     w(f"  const int ni = p.ni, nj = p.nj;")
 
+    def tile_coords(tvar, sfx, indent):
+        """k-plane and tile origin of tile index ``tvar`` (frame variant: the
+        plane's tiles outside the inner rectangle [fi0, fi1) x [fj0, fj1))."""
+        if FRAME:
+            w(f"{indent}const int per{sfx} = tiles_i * tiles_j - (fi1 - fi0) * (fj1 - fj0);")
+            w(f"{indent}const int kk{sfx} = k0 + {tvar} / per{sfx};")
+            w(f"{indent}int ti{sfx}, tj{sfx};")
+            w(f"{indent}gts_frame_tile({tvar} % per{sfx}, tiles_j, fi0, fi1, fj0, fj1, ti{sfx}, tj{sfx});")
+            w(f"{indent}const int i0{sfx} = ti{sfx} * {TI}, j0{sfx} = tj{sfx} * {TJ};")
+        else:
+            w(f"{indent}const int kk{sfx} = k0 + {tvar} / (tiles_i * tiles_j);")
+            w(f"{indent}const int rem{sfx} = {tvar} % (tiles_i * tiles_j);")
+            w(f"{indent}const int i0{sfx} = (rem{sfx} / tiles_j) * {TI}, j0{sfx} = (rem{sfx} % tiles_j) * {TJ};")
+
     def issue(tvar, buf):
         w(f"    {{ const int tt = {tvar};")
-        w("      const int kk_ = k0 + tt / (tiles_i * tiles_j);")
-        w("      const int rem_ = tt % (tiles_i * tiles_j);")
-        w(f"      const int i0_ = (rem_ / tiles_j) * {TI}, j0_ = (rem_ % tiles_j) * {TJ};")
+        tile_coords("tt", "_", "      ")
         w(f"      gts_mbar_arrive_expect_tx(&full[{buf}], {sum(x.box_cols * x.box_rows * x.esize for x in streams)}u);")
         for s in streams:
             w(f"      gts_tma_load_3d(smem + {buf} * {geo.buf_bytes} + {s.smem_off}, &tm_{s.name}, &full[{buf}], "
@@ -423,9 +445,7 @@ def emit(kname: str, plan, kplan, ctype: dict, dtypes: dict, opts=None):
     w("    }")
     w("    gts_mbar_wait(&full[buf], ph);")
     w("    const unsigned char* sb = smem + buf * " + str(geo.buf_bytes) + ";")
-    w("    const int kk = k0 + t / (tiles_i * tiles_j);")
-    w("    const int rem = t % (tiles_i * tiles_j);")
-    w(f"    const int i0 = (rem / tiles_j) * {TI}, j0 = (rem % tiles_j) * {TJ};")
+    tile_coords("t", "", "    ")
     w(f"    const int jl = j0 + lane * {VJ};")
     w(f"    const int ra = i0 + warp * {RI};")
     # per-column store validity
@@ -617,21 +637,40 @@ def emit(kname: str, plan, kplan, ctype: dict, dtypes: dict, opts=None):
             f" {s.box_cols}, {s.box_rows}, 1);",
         ]
     tm_args = ", ".join(f"tm_{kname}_{s.name}" for s in streams)
+    if FRAME:
+        # inner tile rectangle: tiles whose points all lie at least (fr_hi, fr_hj)
+        # inside the domain (they need no halo cell of a field of that extent)
+        tiles = [
+            "      const int tiles_i = (int)((ni + %d) / %d), tiles_j = (int)((nj + %d) / %d);" % (TI - 1, TI, TJ - 1, TJ),
+            "      int fi0 = (fr_hi + %d) / %d, fi1 = ((int)ni - fr_hi) / %d;" % (TI - 1, TI, TI),
+            "      int fj0 = (fr_hj + %d) / %d, fj1 = ((int)nj - fr_hj) / %d;" % (TJ - 1, TJ, TJ),
+            "      if (fi1 < fi0) fi1 = fi0;",
+            "      if (fj1 < fj0) fj1 = fj0;",
+            "      const int nkr = k1 - k0;",
+            "      if (nkr > 0 && tiles_i * tiles_j > (fi1 - fi0) * (fj1 - fj0)) {",
+            "        const int ntiles = (tiles_i * tiles_j - (fi1 - fi0) * (fj1 - fj0)) * nkr;",
+        ]
+        targs = f"{tm_args}, k0, nkr, tiles_i, tiles_j, ntiles, fi0, fi1, fj0, fj1"
+    else:
+        tiles = [
+            f"      const int tiles_i = (int)((ni + {TI - 1}) / {TI}), tiles_j = (int)((nj + {TJ - 1}) / {TJ});",
+            "      const int nkr = k1 - k0;",
+            "      if (nkr > 0) {",
+            "        const int ntiles = tiles_i * tiles_j * nkr;",
+        ]
+        targs = f"{tm_args}, k0, nkr, tiles_i, tiles_j, ntiles"
     launch = [
         "    {",
         f"      const int k0 = {_bound(kplan.interval.start)}, k1 = {_bound(kplan.interval.end)};",
-        f"      const int tiles_i = (int)((ni + {TI - 1}) / {TI}), tiles_j = (int)((nj + {TJ - 1}) / {TJ});",
-        "      const int nkr = k1 - k0;",
-        "      if (nkr > 0) {",
-        "        const int ntiles = tiles_i * tiles_j * nkr;",
+        *tiles,
         "        static bool attr = false;",
         "        static int per_sm = 1;",
         f"        if (!attr) {{ cudaFuncSetAttribute({kname}, cudaFuncAttributeMaxDynamicSharedMemorySize, {smem_bytes});",
         f"          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, {kname}, {32 * NW}, {smem_bytes}); if (per_sm < 1) per_sm = 1; attr = true; }}",
         "        int grid = per_sm * gts_sm_count(); if (grid > ntiles) grid = ntiles;",
-        (f"        gts_launch_pdl({kname}, dim3(grid), dim3({32 * NW}), {smem_bytes}, st, p, {tm_args}, k0, nkr, tiles_i, tiles_j, ntiles);"
+        (f"        gts_launch_pdl({kname}, dim3(grid), dim3({32 * NW}), {smem_bytes}, st, p, {targs});"
          if pdl != "off" else
-         f"        {kname}<<<grid, {32 * NW}, {smem_bytes}, st>>>(p, {tm_args}, k0, nkr, tiles_i, tiles_j, ntiles);"),
+         f"        {kname}<<<grid, {32 * NW}, {smem_bytes}, st>>>(p, {targs});"),
         "      }",
         "    }",
     ]

@@ -53,6 +53,24 @@ GTS_EXPORT int gts_b200_host_alloc(void** ptr, size_t bytes) {
 }
 GTS_EXPORT int gts_b200_host_free(void* ptr) { return (int)cudaFreeHost(ptr); }
 
+// Page-lock an existing host buffer in place (a reference FieldStorage's
+// numpy memory used in mirror mode), so its copies run at full PCIe speed
+// instead of through the driver's pageable staging path.  *registered = 1
+// when this call pinned it, 0 when it was already page-locked (nothing to
+// undo).
+GTS_EXPORT int gts_b200_host_register(void* ptr, size_t bytes, int* registered) {
+  *registered = 0;
+  cudaPointerAttributes attr;
+  if (cudaPointerGetAttributes(&attr, ptr) == cudaSuccess && attr.type == cudaMemoryTypeHost) {
+    return 0;
+  }
+  cudaGetLastError();  // a pageable pointer is not an error
+  const cudaError_t e = cudaHostRegister(ptr, bytes, cudaHostRegisterPortable);
+  if (e == cudaSuccess) *registered = 1;
+  return (int)e;
+}
+GTS_EXPORT int gts_b200_host_unregister(void* ptr) { return (int)cudaHostUnregister(ptr); }
+
 GTS_EXPORT int gts_b200_memset(void* dst, int value, size_t bytes, void* stream) {
   return (int)cudaMemsetAsync(dst, value, bytes, (cudaStream_t)stream);
 }

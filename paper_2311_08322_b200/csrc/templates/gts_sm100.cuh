@@ -179,6 +179,35 @@ __device__ __forceinline__ void gts_tmem_store_f32(uint32_t taddr, float v) {
 }
 
 // ---------------------------------------------------------------------------
+// Frame tiles: the tiles of a tiles_i x tiles_j plane outside the inner
+// rectangle [fi0, fi1) x [fj0, fj1), enumerated row by row (the frame launch
+// of a decomposed step: top rows, then the left / right tiles of the middle
+// rows, then the bottom rows).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void gts_frame_tile(int u, int tiles_j, int fi0, int fi1, int fj0, int fj1,
+                                               int& ti, int& tj) {
+  const int top = fi0 * tiles_j;
+  if (u < top) {
+    ti = u / tiles_j;
+    tj = u - ti * tiles_j;
+    return;
+  }
+  u -= top;
+  const int side = tiles_j - (fj1 - fj0);
+  const int mid = (fi1 - fi0) * side;
+  if (u < mid) {
+    const int r = u / side;
+    const int c = u - r * side;
+    ti = fi0 + r;
+    tj = c < fj0 ? c : c + (fj1 - fj0);
+    return;
+  }
+  u -= mid;
+  ti = fi1 + u / tiles_j;
+  tj = u - (u / tiles_j) * tiles_j;
+}
+
+// ---------------------------------------------------------------------------
 // Programmatic dependent launch (PDL): a persistent stencil kernel lets the
 // next launch in the stream start as soon as every CTA of this one is
 // resident, and waits for the previous grid's completion (and memory flush)
@@ -207,6 +236,7 @@ static cudaError_t gts_launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block,
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  ++g_gts_launches;
   return cudaLaunchKernelEx(&cfg, kern, ((KArgs)args)...);
 }
 

@@ -16,10 +16,12 @@ BACKWARD recurrences run along k).
   packed / unpacked by ``gts_b200_pack_box`` / ``gts_b200_unpack_box``
   kernels on the exchange stream), gloo for host arrays (used by the CPU
   tests of this logic).
-* ``overlap_call`` -- runs a stencil on the interior (which needs no halo)
-  while the exchange is in flight, then on the four boundary strips; every
-  point is computed by exactly the same instructions as in an undecomposed
-  run, so the result is bitwise identical.
+* ``DecomposedStep`` -- runs a stencil on the interior (which needs no halo)
+  while the exchange is in flight, then ONE frame launch over the tiles
+  touching the halo-dependent band (``split_launches``; the four boundary
+  strips for stencils without a frame launch); every point is computed by
+  exactly the same instructions as in an undecomposed run, so the result is
+  bitwise identical.
 """
 
 from __future__ import annotations
@@ -259,53 +261,123 @@ def call_on_strip(stencil, fields: dict, scalars: dict, offset: tuple, size: tup
     stencil(domain=tuple(size), origin=origins, **fields, **scalars)
 
 
+def split_launches(module, domain: tuple, halo: tuple, fields: dict, scalars: dict, stream: int,
+                   has_neighbours: bool):
+    """(interior launchers, boundary launchers) of one decomposed step.
+
+    Without neighbours: one launch of the whole local domain.  Otherwise the
+    interior box [hi, ni-hi) x [hj, nj-hj) (no halo cell read) runs while the
+    halo is in flight, and the rest after it lands:
+
+    * ONE frame launch when the module supports it (a single fused PARALLEL
+      kernel whose recomputation is idempotent, codegen ``frame_ok``): the
+      whole domain, enumerating only the thin tiles that touch the band
+      (Module.frame_launcher) -- 2 launches per step;
+    * otherwise the four boundary strips (5 launches per step)."""
+    if not has_neighbours:
+        return [module.launcher(domain, fields, scalars, stream)], []
+    parts = strips(domain, halo)
+    interior = [module.launcher(size, fields, scalars, stream, (off[0], off[1], 0))
+                for name, off, size in parts if name in ("interior", "all")]
+    if module.frame_supported and any(name == "interior" for name, _, _ in parts):
+        boundary = [module.frame_launcher(domain, fields, scalars, stream, halo)]
+    else:
+        boundary = [module.launcher(size, fields, scalars, stream, (off[0], off[1], 0))
+                    for name, off, size in parts if name not in ("interior", "all")]
+    return interior, boundary
+
+
+class _GraphReplay:
+    """``steps`` steps of a decomposed step replayed from one CUDA graph, or
+    (``graph=None``: the capture was refused, e.g. by a NCCL build without
+    stream-capture support) re-enqueued eagerly step by step."""
+
+    def __init__(self, step, graph, steps: int, written: list):
+        self.step, self.graph, self.steps, self.written = step, graph, steps, written
+
+    def launch(self) -> None:
+        if self.graph is not None:
+            self.graph.launch()
+        else:
+            for _ in range(self.steps):
+                self.step()
+        for w in self.written:  # storages written by the replay: host mirrors are stale
+            w.mark_device_written(self.step.compute)
+
+
 class DecomposedStep:
     """One time step of a PARALLEL stencil on a decomposed domain, fully
-    asynchronous: the halo exchange of ``halo_field`` (pack -> NCCL
-    send/recv -> unpack on a communication stream) overlaps the interior of
-    the local domain on the compute stream; the four boundary strips run once
-    the halos have landed.  No host synchronisation inside the step."""
+    asynchronous, in 2 stencil launches: the halo exchange of ``halo_field``
+    (pack -> NCCL send/recv -> unpack on the communication stream) overlaps
+    the interior launch on the compute stream; the frame launch
+    (``split_launches``) runs once the halos have landed.  No host
+    synchronisation inside the step, and ``graph(n)`` captures n steps --
+    the NCCL calls included -- into one CUDA graph."""
 
     def __init__(self, stencil, decomposition: Decomposition, fields: dict, scalars: dict,
-                 halo_field: str, halo: tuple):
+                 halo_field: str, halo: tuple, split: Optional[bool] = None):
+        """``split``: interior + frame launches even without neighbours (the
+        1-GPU measurement of what the split costs; default: only with
+        neighbours)."""
         import torch
 
         from . import native
 
-        self.torch = torch
-        self.compute = torch.cuda.ExternalStream(native.default_stream())
-        self.comm = torch.cuda.Stream()
+        self.torch, self.native = torch, native
+        self.compute = self.stream = native.default_stream()
+        self.comm = native.aux_stream("nccl-halo")
         self.decomp = decomposition
-        module = stencil.build_info["module"]
+        self.module = stencil.build_info["module"]
+        self.fields = fields
         dom = decomposition.local_domain
         has_nb = any(decomposition.neighbour(di, dj) is not None
                      for di, dj in ((-1, 0), (1, 0), (0, -1), (0, 1)))
         self.exchanger = None
         if has_nb:
             self.exchanger = HaloExchanger(decomposition, halo, fields[halo_field].dtype, device=True,
-                                           stream=self.comm.cuda_stream)
+                                           stream=self.comm)
             self.field = fields[halo_field]
-            parts = strips(dom, halo)
-        else:
-            parts = [("all", (0, 0), dom)]
-        cs = self.compute.cuda_stream
-        self.interior = [module.launcher(size, fields, scalars, cs, (off[0], off[1], 0))
-                         for name, off, size in parts if name in ("interior", "all")]
-        self.boundary = [module.launcher(size, fields, scalars, cs, (off[0], off[1], 0))
-                         for name, off, size in parts if name not in ("interior", "all")]
+            self._comm_t = torch.cuda.ExternalStream(self.comm)
+        self.interior, self.boundary = split_launches(self.module, dom, halo, fields, scalars, self.compute,
+                                                      has_nb if split is None else split)
         self.launches_per_step = len(self.interior) + len(self.boundary)
+        self._ev_start, self._ev_halo = native.Event(), native.Event()
 
     def __call__(self) -> None:
+        n = self.native
         if self.exchanger is not None:
-            self.comm.wait_stream(self.compute)
-            with self.torch.cuda.stream(self.comm):
+            self._ev_start.record_dep(self.compute)  # the field is final for this step
+            n.call("gts_b200_stream_wait_event", self.comm, self._ev_start.ptr)
+            with self.torch.cuda.stream(self._comm_t):
                 self.exchanger.exchange_async(self.field)
+            self._ev_halo.record_dep(self.comm)
         for go in self.interior:
             go()
         if self.exchanger is not None:
-            self.compute.wait_stream(self.comm)
+            n.call("gts_b200_stream_wait_event", self.compute, self._ev_halo.ptr)
         for go in self.boundary:
             go()
+        if self.exchanger is not None:
+            self.field.mark_device_written(self.compute)  # halo rewritten (joined into compute)
+
+    def graph(self, steps: int) -> _GraphReplay:
+        """``steps`` steps captured into one CUDA graph on the compute stream
+        (the communication stream joins through the fork / join events; NCCL
+        send / recv are stream-capturable).  If the capture is refused the
+        replay falls back to eager enqueues."""
+        written = [self.fields[name] for name in self.module.written]
+        if self.exchanger is not None:
+            written.append(self.field)  # its halo is rewritten by the unpack
+        g = self.native.Graph(self.compute)
+        try:
+            with g.capture():
+                for _ in range(steps):
+                    self()
+        except Exception:  # noqa: BLE001 - capture refused: eager replay
+            self.native.synchronize(self.compute)
+            self.native.synchronize(self.comm)
+            return _GraphReplay(self, None, steps, written)
+        return _GraphReplay(self, g, steps, written)
 
 
 # ---------------------------------------------------------------------------
@@ -484,12 +556,8 @@ class PeerDecomposedStep:
         self.exchanger = PeerHaloExchanger(decomposition, halo, fields[halo_field], self.comm, group)
         self.fields = fields
         self.written = sorted(module.written)
-        parts = strips(dom, halo) if self.exchanger.peer else [("all", (0, 0), dom)]
-        cs = self.compute
-        self.interior = [module.launcher(size, fields, scalars, cs, (off[0], off[1], 0))
-                         for name, off, size in parts if name in ("interior", "all")]
-        self.boundary = [module.launcher(size, fields, scalars, cs, (off[0], off[1], 0))
-                         for name, off, size in parts if name not in ("interior", "all")]
+        self.interior, self.boundary = split_launches(module, dom, halo, fields, scalars, self.compute,
+                                                      bool(self.exchanger.peer))
         self.launches_per_step = len(self.interior) + len(self.boundary)
         self._ev_start, self._ev_halo = native.Event(), native.Event()
 

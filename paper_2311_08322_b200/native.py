@@ -36,6 +36,8 @@ SIGNATURES = {
     "gts_b200_free": (_INT, [_VP]),
     "gts_b200_host_alloc": (_INT, [_c.POINTER(_VP), _SZ]),
     "gts_b200_host_free": (_INT, [_VP]),
+    "gts_b200_host_register": (_INT, [_VP, _SZ, _c.POINTER(_INT)]),
+    "gts_b200_host_unregister": (_INT, [_VP]),
     "gts_b200_memset": (_INT, [_VP, _INT, _SZ, _VP]),
     "gts_b200_memcpy_h2d": (_INT, [_VP, _VP, _SZ, _VP]),
     "gts_b200_memcpy_d2h": (_INT, [_VP, _VP, _SZ, _VP]),
@@ -151,9 +153,6 @@ def call(name: str, *args) -> None:
 # Devices and streams
 # ---------------------------------------------------------------------------
 
-_streams: dict = {}
-
-
 def device_count() -> int:
     n = ctypes.c_int(0)
     st = lib().gts_b200_device_count(ctypes.byref(n))
@@ -176,29 +175,64 @@ def require_device() -> int:
     return current_device()
 
 
-_aux_streams: dict = {}
+class _ThreadStreams:
+    """The calling thread's backend streams on one device.  Threads get
+    their own streams so concurrent calls never share a stream,
+    a temporary arena (gts_common.cuh ``GtsArenaLease``, keyed by stream) or
+    a mirror buffer; a finished thread's streams go back to a pool."""
+
+    _pool: dict = {}  # (device, name) -> [free stream handles]
+    _pool_lock = threading.Lock()
+
+    def __init__(self, dev: int):
+        self.dev = dev
+        self.streams: dict = {}
+
+    def get(self, name: str) -> int:
+        s = self.streams.get(name)
+        if s is None:
+            with _ThreadStreams._pool_lock:
+                free = _ThreadStreams._pool.get((self.dev, name))
+                s = free.pop() if free else None
+            if s is None:
+                p = ctypes.c_void_p()
+                call("gts_b200_stream_create", ctypes.byref(p))
+                s = p.value
+            self.streams[name] = s
+        return s
+
+    def __del__(self):  # pragma: no cover - thread teardown
+        try:
+            with _ThreadStreams._pool_lock:
+                for name, s in self.streams.items():
+                    _ThreadStreams._pool.setdefault((self.dev, name), []).append(s)
+        except Exception:
+            pass
+
+
+_tls = threading.local()
+
+
+def _thread_streams(dev: int) -> _ThreadStreams:
+    per = getattr(_tls, "streams", None)
+    if per is None:
+        per = _tls.streams = {}
+    ts = per.get(dev)
+    if ts is None:
+        ts = per[dev] = _ThreadStreams(dev)
+    return ts
 
 
 def aux_stream(name: str) -> int:
-    """Extra non-blocking streams per device (the mirror-mode copy engines)."""
-    dev = require_device()
-    s = _aux_streams.get((dev, name))
-    if s is None:
-        p = ctypes.c_void_p()
-        call("gts_b200_stream_create", ctypes.byref(p))
-        s = _aux_streams[(dev, name)] = p.value
-    return s
+    """Extra non-blocking streams of the calling thread (the mirror-mode
+    copy engines, the halo exchange)."""
+    return _thread_streams(require_device()).get("aux:" + name)
 
 
 def default_stream() -> int:
-    """One non-blocking stream per device, owned by the backend."""
-    dev = require_device()
-    s = _streams.get(dev)
-    if s is None:
-        p = ctypes.c_void_p()
-        call("gts_b200_stream_create", ctypes.byref(p))
-        s = _streams[dev] = p.value
-    return s
+    """The calling thread's non-blocking stream on the current device, owned
+    by the backend."""
+    return _thread_streams(require_device()).get("default")
 
 
 def synchronize(stream: Optional[int] = None) -> None:

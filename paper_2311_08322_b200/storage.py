@@ -10,8 +10,16 @@ written against the reference (``storage.view[...] = values``,
 
 * reading ``view`` / ``data()`` first copies device -> host if the device
   copy is newer, and marks the host mirror as possibly modified;
-* the next stencil call copies host -> device before launching if the host
-  mirror may have been modified.
+* every launch (a stencil call, a ``Module.launcher`` enqueue, a TimeLoop or
+  graph replay) first copies host -> device if the host mirror may have been
+  modified, so the device copy is never newer than a pending host write and
+  the two flags are never both set;
+* an asynchronous launch remembers its stream: a later host read, or a
+  launch on another stream, waits for it first.
+
+Synchronisation takes a per-storage lock, so threads sharing an input storage
+(concurrent calls on disjoint outputs) upload it once, and no
+thread launches on it before the upload completed.
 
 The b200 layout is the gen engine's axis order (k outermost, j contiguous,
 ``storage.py:60-64``) with the origin element and every row aligned to
@@ -21,6 +29,7 @@ The b200 layout is the gen engine's axis order (k outermost, j contiguous,
 from __future__ import annotations
 
 import ctypes
+import threading
 import weakref
 from typing import Optional, Union
 
@@ -117,6 +126,8 @@ class DeviceFieldStorage(FieldStorage):
         self._base = host_flat
         self._host_dirty = True  # nothing uploaded yet
         self._device_dirty = False
+        self._pending_stream = None  # stream of an asynchronous write not yet waited for
+        self._sync_lock = threading.RLock()
 
     # -- FieldStorage surface ------------------------------------------------
     @property
@@ -142,24 +153,48 @@ class DeviceFieldStorage(FieldStorage):
         return self._buf.hptr + self._hshift * self.itemsize
 
     def to_device(self, stream: Optional[int] = None, sync: bool = True) -> None:
-        if self._host_dirty:
-            s = native.default_stream() if stream is None else stream
-            native.call("gts_b200_memcpy_h2d", self.base_address(), self._host_span_addr(),
-                        self.nbytes_span, s)
-            if sync:
-                native.synchronize(s)
-            self._host_dirty = False
+        """Upload a pending host write (``sync=False``: the copy stays queued
+        on ``stream``, so only launches on that same stream may follow
+        without a wait; used inside a single-threaded graph capture)."""
+        if not self._host_dirty:
+            return
+        with self._sync_lock:
+            if self._host_dirty:
+                s = native.default_stream() if stream is None else stream
+                native.call("gts_b200_memcpy_h2d", self.base_address(), self._host_span_addr(),
+                            self.nbytes_span, s)
+                if sync:
+                    native.synchronize(s)
+                self._host_dirty = False
 
     def to_host(self, stream: Optional[int] = None) -> None:
-        if self._device_dirty:
-            s = native.default_stream() if stream is None else stream
-            native.call("gts_b200_memcpy_d2h", self._host_span_addr(), self.base_address(),
-                        self.nbytes_span, s)
-            native.synchronize(s)
-            self._device_dirty = False
+        if not self._device_dirty:
+            return
+        with self._sync_lock:
+            if self._device_dirty:
+                s = native.default_stream() if stream is None else stream
+                pend = self._pending_stream
+                if pend is not None and pend != s:
+                    native.synchronize(pend)
+                native.call("gts_b200_memcpy_d2h", self._host_span_addr(), self.base_address(),
+                            self.nbytes_span, s)
+                native.synchronize(s)
+                self._device_dirty = False
+                self._pending_stream = None
 
-    def mark_device_written(self) -> None:
+    def mark_device_written(self, stream: Optional[int] = None) -> None:
+        """A launch wrote the device copy: asynchronously on ``stream``
+        (not yet synchronised), or ``None`` for a completed write."""
         self._device_dirty = True
+        self._pending_stream = stream
+
+    def wait_producer(self, stream: int) -> None:
+        """Order ``stream`` after the last asynchronous write of another
+        stream (host-side wait; the common single-stream case costs nothing)."""
+        pend = self._pending_stream
+        if pend is not None and pend != stream:
+            native.synchronize(pend)
+            self._pending_stream = None
 
     def host_array(self) -> np.ndarray:
         """Synchronised read-only copy of the logical array (no dirty mark)."""
@@ -219,6 +254,9 @@ class ExternalDeviceFieldStorage(DeviceFieldStorage):
         stream = cai.get("stream")
         if stream:  # v3: work queued on the producer's stream must finish first
             native.call("gts_b200_stream_synchronize", int(stream))
+        self._sync_lock = threading.RLock()
+        self._pending_stream = None
+        self._ev = None
         self.device = native.require_device()
         self._ext, self._ptr = obj, int(ptr)
         total = 1 + sum((n - 1) * st for n, st in zip(shape, strides))
@@ -242,6 +280,34 @@ class ExternalDeviceFieldStorage(DeviceFieldStorage):
 
     def _host_span_addr(self) -> int:
         return self._host.hptr
+
+    @property
+    def view(self) -> np.ndarray:  # type: ignore[override]
+        """Read-only host snapshot: the device array is the authoritative
+        copy (write to the producer's array, e.g. the torch tensor, instead);
+        the host mirror is never uploaded over it."""
+        self.to_host()
+        v = self._host_view.view()
+        v.flags.writeable = False
+        return v
+
+    @view.setter
+    def view(self, value) -> None:  # pragma: no cover - dataclass compatibility
+        raise AttributeError("ExternalDeviceFieldStorage.view is read-only")
+
+    def wait_producer(self, stream: int) -> None:
+        """Order ``stream`` after the work the array's producer has queued
+        on ITS current stream (``__cuda_array_interface__`` v3 ``stream``,
+        re-read on every launch: a torch tensor reports the torch current
+        stream), without a host wait."""
+        super().wait_producer(stream)
+        cai = getattr(self._ext, "__cuda_array_interface__", None) or {}
+        prod = cai.get("stream")
+        if prod and int(prod) != stream:
+            if self._ev is None:
+                self._ev = native.Event()
+            native.call("gts_b200_event_record", self._ev.ptr, int(prod))
+            native.call("gts_b200_stream_wait_event", stream, self._ev.ptr)
 
 
 def from_cuda_array(obj, origin=(0, 0, 0)) -> ExternalDeviceFieldStorage:

@@ -25,7 +25,7 @@ from __future__ import annotations
 from typing import Optional, Sequence
 
 from . import native
-from ._host import InvocationError, sf_runtime
+from ._host import Code, InvocationError, sf_runtime
 from .storage import DeviceFieldStorage
 
 
@@ -36,9 +36,10 @@ class TimeLoop:
         ``bindings``: field dicts {name: DeviceFieldStorage}, one per phase of
         the rotation; ``scalars``: api scalars shared by every step."""
         if stencil.backend != "b200":
-            raise InvocationError(f"TimeLoop needs a b200 stencil, got backend '{stencil.backend}'")
+            raise InvocationError(Code.UNKNOWN_BACKEND,
+                                  f"TimeLoop needs a b200 stencil, got backend '{stencil.backend}'")
         if steps < 1 or not bindings:
-            raise InvocationError("TimeLoop needs steps >= 1 and at least one binding")
+            raise InvocationError(Code.MISSING_ARGUMENT, "TimeLoop needs steps >= 1 and at least one binding")
         self.stencil = stencil
         self.module = stencil.executable.build_info["module"]
         self.steps = int(steps)
@@ -50,7 +51,8 @@ class TimeLoop:
         for fields in bindings:
             for name, st in fields.items():
                 if not isinstance(st, DeviceFieldStorage):
-                    raise InvocationError(f"TimeLoop field '{name}' must be a DeviceFieldStorage")
+                    raise InvocationError(Code.LAYOUT_MISMATCH,
+                                          f"TimeLoop field '{name}' must be a DeviceFieldStorage")
             # the reference's own argument resolution and validation
             # (runtime.py:122-217), once per binding
             args = {f.name: fields[f.name] for f in impl.api_fields}
@@ -59,14 +61,15 @@ class TimeLoop:
             if self.domain is None:
                 self.domain = tuple(dom)
             elif tuple(dom) != self.domain:
-                raise InvocationError(f"bindings resolve to different domains {self.domain} / {tuple(dom)}")
+                raise InvocationError(Code.OUT_OF_BOUNDS,
+                                      f"bindings resolve to different domains {self.domain} / {tuple(dom)}")
             offset_ok = all(tuple(origins[n]) == tuple(fields[n].origin) for n in fields)
             if not offset_ok:
-                raise InvocationError("TimeLoop uses the storages' own origins")
+                raise InvocationError(Code.OUT_OF_BOUNDS, "TimeLoop uses the storages' own origins")
             self.launchers.append(self.module.launcher(self.domain, fields, scalars, self.stream))
         self.bindings = list(bindings)
         self._graph = None
-        self.launches_per_step = len(self.module.plan.kernels)
+        self.launches_per_step = None  # counted when the steps are captured
 
     def _enqueue(self) -> None:
         for s in range(self.steps):
@@ -82,8 +85,12 @@ class TimeLoop:
                 for st in fields.values():
                     st.to_device(self.stream)
             g = native.Graph(self.stream)
+            n0 = self.module.launch_count()
             with g.capture():
                 self._enqueue()
+            # kernels per step as enqueued by the module's entry (the plan
+            # may fuse several kernels into one launch)
+            self.launches_per_step = (self.module.launch_count() - n0) / self.steps
             self._graph = g
         return self
 
@@ -95,14 +102,25 @@ class TimeLoop:
         self._mark_written()
 
     def run(self, sync: bool = True) -> None:
-        """All ``steps`` steps: one graph launch (captured on first use)."""
+        """All ``steps`` steps: one graph launch (captured on first use).
+        Host writes made through ``.view`` since the last launch are
+        uploaded first, so the replay never works on (and then hides) a
+        stale device copy."""
         self.capture()
+        self._upload_pending()
         self._graph.launch()
         self._mark_written()
         if sync:
             native.synchronize(self.stream)
 
+    def _storages(self):
+        return list({id(st): st for fields in self.bindings for st in fields.values()}.values())
+
+    def _upload_pending(self) -> None:
+        for st in self._storages():
+            st.to_device(self.stream)
+            st.wait_producer(self.stream)
+
     def _mark_written(self) -> None:
-        for fields in self.bindings:
-            for st in fields.values():
-                st._device_dirty = True
+        for st in self._storages():
+            st.mark_device_written(self.stream)

@@ -150,7 +150,10 @@ class BuildCache:
                 os.rename(tmp, self.entry_dir(fp))
             except OSError:
                 if self.lookup(fp) is None:
-                    raise
+                    # a stale entry without its object (a crashed or pruned
+                    # build): replace it, still by one atomic rename
+                    self.evict(fp)
+                    os.rename(tmp, self.entry_dir(fp))
         finally:
             shutil.rmtree(tmp, ignore_errors=True)
         return self.so_path(fp)

@@ -30,6 +30,26 @@ stencil hdiff(inp: Field[f64], coeff: f64, out: Field[f64]):
 """
 
 
+# every DSL builtin (ir.BUILTINS) in one stencil: tests/golden/make_golden_builtins.py
+BUILTIN_OUTS = ["o_abs", "o_min", "o_max", "o_sqrt", "o_exp", "o_log", "o_pow", "o_floor", "o_ceil"]
+BUILTINS_SRC = """
+stencil builtins(x: Field[f64], y: Field[f64], o_abs: Field[f64], o_min: Field[f64], o_max: Field[f64],
+                 o_sqrt: Field[f64], o_exp: Field[f64], o_log: Field[f64], o_pow: Field[f64],
+                 o_floor: Field[f64], o_ceil: Field[f64]):
+    with computation(PARALLEL):
+        with interval(0, None):
+            o_abs = abs(x)
+            o_min = min(x, y)
+            o_max = max(x, y)
+            o_sqrt = sqrt(x)
+            o_exp = exp(x)
+            o_log = log(x)
+            o_pow = pow(x, y)
+            o_floor = floor(x)
+            o_ceil = ceil(x)
+"""
+
+
 def field_halo(extent) -> tuple:
     """corpus.py:236-237."""
     return tuple(max(-lo, hi) for lo, hi in zip(extent.lo, extent.hi))

@@ -326,11 +326,8 @@ def test_mirror_stores_exact_cells_single_process():
             j0, j1 = {-1: (0, 2), 0: (0, nj), 1: (nj - 2, nj)}[dj]
             boxes.append((i0, i1, j0, j1, scratch.base_address() + org, *scratch.strides))
     mod = st_m.build_info["module"]
-    try:
-        mod.set_mirror(boxes)
-        st_m(u_in=u, u_out=out_m, **coef, **sc)
-    finally:
-        mod.set_mirror([])
+    mod.set_mirror(boxes)  # for the next launch only (consumed by it)
+    st_m(u_in=u, u_out=out_m, **coef, **sc)
     st_p(u_in=u, u_out=out_p, **coef, **sc)
     native.synchronize(native.default_stream())
     scratch.mark_device_written()
@@ -343,6 +340,14 @@ def test_mirror_stores_exact_cells_single_process():
     assert np.array_equal(s[band], o[band])
     assert np.all(s[~band] == -7.0)
     assert np.all(scratch.host_array()[:2] == -7.0) and np.all(scratch.host_array()[:, :2] == -7.0)
+    # the boxes were consumed by that launch: a later plain call of the same
+    # module stores nothing outside its own output (no stale peer
+    # pointers after PeerFusedStep.close())
+    scratch.view[...] = -9.0
+    scratch.to_device()
+    st_m(u_in=u, u_out=out_m, **coef, **sc)
+    scratch.mark_device_written()  # re-read the device copy below
+    assert np.all(scratch.host_array() == -9.0)
 
 
 @pytest.mark.parametrize("grid", [(2, 2), (3, 3), (4, 2)])
@@ -429,3 +434,49 @@ def test_fused_step_protocol_model(nranks):
             for x in range(nranks):
                 for n in nbs[x]:
                     assert not (state[x] == "run" and state[n] == "run" and abs(step[x] - step[n]) == 1), seed
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dom", [(512, 1024, 6), (37, 300, 3), (70, 33, 2), (5, 200, 2), (3, 3, 2)])
+def test_interior_plus_frame_launch_bitwise(dom):
+    """decomp.split_launches on one GPU: the interior box launch + ONE frame
+    launch (thin tiles touching the 2-deep band) compute every point exactly
+    like the single full launch (bitwise vs the oracle, output poisoned
+    first); the frame launch alone writes the whole band."""
+    import numpy as np
+
+    import oracle
+    import paper_2311_08322_b200 as b200
+    from paper_2311_08322_b200 import decomp, native, workloads
+
+    st = b200.compile_stencil(workloads.source("hdiff"), "hdiff")
+    module = st.build_info["module"]
+    assert module.frame_supported
+    vals = np.random.default_rng(sum(dom)).uniform(-1, 1, (dom[0] + 4, dom[1] + 4, dom[2]))
+    want = oracle.hdiff_c(vals, 0.05)
+    inp = b200.from_array(vals, (2, 2, 0))
+    stream = native.default_stream()
+    out = b200.allocate("f64", dom, fill="poison")
+    fields = {"inp": inp, "out": out}
+    interior, boundary = decomp.split_launches(module, dom, (2, 2), fields, {"coeff": 0.05}, stream, True)
+    has_interior = dom[0] > 4 and dom[1] > 4
+    assert len(interior) == 1 and len(boundary) == (1 if has_interior else 0)
+    n0 = module.launch_count()
+    for go in interior + boundary:
+        go()
+    native.synchronize(stream)
+    assert module.launch_count() - n0 == len(interior) + len(boundary)
+    assert np.array_equal(out.host_array(), want)
+    if has_interior:
+        out2 = b200.allocate("f64", dom, fill="poison")
+        fields2 = {"inp": inp, "out": out2}
+        _, frame = decomp.split_launches(module, dom, (2, 2), fields2, {"coeff": 0.05}, stream, True)
+        frame[0]()
+        native.synchronize(stream)
+        got = out2.host_array()
+        band = np.ones(dom, bool)
+        band[2:-2, 2:-2, :] = False
+        assert np.array_equal(got[band], want[band])
+        # interior points are either untouched (poison) or the same values
+        inner = got[~band]
+        assert np.all(np.isnan(inner) | (inner == want[~band]))

@@ -96,3 +96,54 @@ def test_dycore_launch_paths_match_golden(gpu, opts, align):
         src, dst = bufs[s % 2], bufs[(s + 1) % 2]
         st(u_in=src, u_out=dst, **coef, **workloads.DYCORE_SCALARS)
         assert np.array_equal(dst.host_array()[2:-2, 2:-2, :], g[f"{key}_out{s}"]), (opts, align, s)
+
+
+@pytest.mark.gpu
+def test_dycore_configs4_size_100_steps_vs_reference_kernel(gpu):
+    """BASELINE configs[4] at full size: 512x512x80 f64, 100 time steps in one
+    CUDA-graph TimeLoop replay, bitwise against the reference gen engine's own
+    kernel for dycore.gts (oracle/_ref, 100 host-swapped calls); the first 10
+    steps also against the independent C restatement (oracle.dycore_run)."""
+    import paper_2311_08322_b200 as b200
+    from paper_2311_08322_b200 import workloads
+    from paper_2311_08322_b200.timeloop import TimeLoop
+
+    if not oracle.ref_available("dycore_f64"):
+        pytest.fail("oracle/_ref/libdycore_f64.so missing: run __graft_entry__.build() in the build container")
+    dom = (512, 512, 80)
+    arr, bufs, coef = _state(dom, 1000)
+    st = b200.compile_stencil(workloads.source("dycore"), "dycore")
+    A, B = bufs
+    binds = [dict(u_in=A, u_out=B, **coef), dict(u_in=B, u_out=A, **coef)]
+    TimeLoop(st, binds, 10, workloads.DYCORE_SCALARS).run()
+    want10 = oracle.dycore_run(arr["u"], arr["a"], arr["b"], arr["c"], 10)
+    assert np.array_equal(A.host_array(), want10)
+    TimeLoop(st, binds, 90, workloads.DYCORE_SCALARS).run()
+    want100 = oracle.ref_dycore_run(want10, arr["a"], arr["b"], arr["c"], 90)
+    got = A.host_array()
+    assert np.isfinite(got).all()
+    assert np.array_equal(got, want100), oracle.max_rel(got, want100)
+
+
+@pytest.mark.gpu
+def test_timeloop_host_write_after_view_is_not_lost(gpu):
+    """reading ``.view`` (host-dirty) and then replaying a TimeLoop
+    must not let a later call upload the stale host mirror over the newer
+    device state: the replay uploads pending host data first."""
+    import paper_2311_08322_b200 as b200
+    from paper_2311_08322_b200 import workloads
+    from paper_2311_08322_b200.timeloop import TimeLoop
+
+    dom = (40, 36, 12)
+    arr, (A, B), coef = _state(dom, 8)
+    st = b200.compile_stencil(workloads.source("dycore"), "dycore")
+    loop = TimeLoop(st, [dict(u_in=A, u_out=B, **coef), dict(u_in=B, u_out=A, **coef)], 2,
+                    workloads.DYCORE_SCALARS)
+    loop.run()
+    _ = A.view[0, 0, 0]  # marks A host-dirty (the caller may write through it)
+    _ = B.view[0, 0, 0]
+    loop.run()
+    st(u_in=A, u_out=B, **coef, **workloads.DYCORE_SCALARS)  # a plain call after the replay
+    want = oracle.dycore_run(arr["u"], arr["a"], arr["b"], arr["c"], 5)
+    assert np.array_equal(B.host_array(), want)
+    assert loop.launches_per_step == 1  # the fused TMEM kernel: one launch per step

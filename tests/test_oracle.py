@@ -85,7 +85,29 @@ def test_reference_ref_kernels_present_or_skipped():
     if not man.exists():
         pytest.skip("oracle/_ref not built here")
     m = json.loads(man.read_text())
-    assert set(m) == {"hdiff_f64", "hdiff_f32", "vadv_f64", "vadv_f32"}
+    assert set(m) == {"hdiff_f64", "hdiff_f32", "vadv_f64", "vadv_f32", "dycore_f64"}
+
+
+def test_reference_ref_kernels_match_goldens(golden):
+    """The reference's own kernels (the full-size checker of bench.py and the
+    GPU tests) reproduce the golden vectors of its vec / debug engines."""
+    if not oracle.ref_available("hdiff_f64"):
+        pytest.skip("oracle/_ref not built here")
+    for key in _cases(golden, "hdiff_"):
+        got = oracle.ref_hdiff(golden[key + "_inp"], 0.05)
+        assert np.array_equal(got, golden[key + "_out"]), key
+    for key in _cases(golden, "vadv_"):
+        got = oracle.ref_vadv(*(golden[f"{key}_{n}"] for n in "abcd"))
+        assert np.array_equal(got, golden[key + "_x"]), key
+    from paper_2311_08322_b200 import workloads
+
+    g, keys = _dycore_cases()
+    for key in keys:
+        dom = tuple(int(x) for x in key.split("_")[1].split("x"))
+        u, a, b, c = (workloads.dycore_arrays(dom, int(g[key + "_seed"]))[n] for n in "uabc")
+        for s in range(int(g[key + "_steps"])):
+            got = oracle.ref_dycore_run(u, a, b, c, s + 1)[2:-2, 2:-2, :]
+            assert np.array_equal(got, g[f"{key}_out{s}"]), (key, s)
 
 
 def _dycore_cases():

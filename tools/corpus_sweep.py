@@ -8,7 +8,10 @@ the reference harness inputs (tests/_inputs.py restatement of
 corpus.random_field_args) and compares SHA-256 of every output compute view
 with the reference debug engine's (tests/golden/corpus.json).  Also runs
 each program through three launch configurations (default, no fusion, no
-TMEM) to cover every lowering path.
+TMEM) to cover every lowering path, and (``tiles``) at the two tile-crossing
+domains of tests/golden/corpus_tiles.json -- (37, 300, 9) and (70, 260, 120),
+several fused / column tiles in i and j -- against the reference vec
+engine's output hashes.
 """
 import json
 import os
@@ -55,8 +58,18 @@ def main():
     print(json.dumps(sweep(n), indent=1))
 
 
-def sweep(n: int = 200, configs=None) -> dict:
+def _run_one(b200, _inputs, np, st, dom, seed, scalars, outputs, want_sha) -> str:
+    arrays = _inputs.random_field_arrays(st.implementation, dom, np.random.default_rng(seed))
+    fields = {k: b200.from_array(a, o) for k, (a, o) in arrays.items()}
+    st(domain=dom, **fields, **scalars)
+    ok = all(_inputs.sha(_inputs.compute_view(fields[o].host_array(), fields[o].origin, dom))
+             == want_sha[o] for o in outputs)
+    return "bitwise" if ok else "MISMATCH"
+
+
+def sweep(n: int = 200, configs=None, tiles: bool = True) -> dict:
     meta = json.loads((REPO / "tests" / "golden" / "corpus.json").read_text())[:n]
+    tile_meta = json.loads((REPO / "tests" / "golden" / "corpus_tiles.json").read_text())[:n] if tiles else []
     cfgs = range(len(OPTS)) if configs is None else configs
     jobs = [(e["idx"], e["source"], e["name"], oi) for e in meta for oi in cfgs]
     t0 = time.time()
@@ -78,14 +91,20 @@ def sweep(n: int = 200, configs=None) -> dict:
                 results.append(rec)
                 continue
             st = b200.compile_stencil(e["source"], e["name"], cache_dir=CACHE, gen_options=OPTS[oi])
-            dom = tuple(e["domain"])
-            arrays = _inputs.random_field_arrays(st.implementation, dom, np.random.default_rng(e["seed"]))
-            fields = {k: b200.from_array(a, o) for k, (a, o) in arrays.items()}
+            runs = [(tuple(e["domain"]), e["seed"], e["scalars"], e["output_sha"])]
+            if tiles:
+                tm = tile_meta[e["idx"]]
+                assert tm["name"] == e["name"]
+                runs += [(tuple(r["domain"]), r["seed"], r["scalars"], r["output_sha"]) for r in tm["runs"]]
+            rec["domains"] = {}
             try:
-                st(domain=dom, **fields, **e["scalars"])
-                ok = all(_inputs.sha(_inputs.compute_view(fields[o].host_array(), fields[o].origin, dom))
-                         == e["output_sha"][o] for o in e["outputs"])
-                rec["status"] = "bitwise" if ok else "MISMATCH"
+                for dom, seed, scalars, want in runs:
+                    rec["domains"][str(dom)] = _run_one(b200, _inputs, np, st, dom, seed, scalars,
+                                                        e["outputs"], want)
+                bad = [d for d, v in rec["domains"].items() if v != "bitwise"]
+                rec["status"] = "MISMATCH" if bad else "bitwise"
+                if bad:
+                    rec["mismatch_domains"] = bad
             except Exception as exc:
                 rec["status"] = "run_error"
                 rec["error"] = f"{type(exc).__name__}: {exc}"[:300]
@@ -93,7 +112,7 @@ def sweep(n: int = 200, configs=None) -> dict:
                 kinds[k.split(":")[0]] = kinds.get(k.split(":")[0], 0) + 1
             results.append(rec)
     summary = {"programs": len(meta), "configs": len(list(cfgs)), "compile_s": round(t_comp, 1),
-               "status": {}, "kernel_kinds": kinds}
+               "domains_per_program": 1 + (2 if tiles else 0), "status": {}, "kernel_kinds": kinds}
     for r in results:
         summary["status"][r["status"]] = summary["status"].get(r["status"], 0) + 1
     return {"summary": summary, "failures": [r for r in results if r["status"] != "bitwise"]}
