@@ -104,6 +104,13 @@ int gts_b200_event_elapsed_ms(float* ms, void* start, void* end);
 /* Evict L2 between timed iterations by writing a buffer of 2x the L2 size
  * on the given stream (SURVEY.md 8(d) timing protocol). */
 int gts_b200_l2_flush(void* stream);
+/* read-only eviction of the L2 (2x L2 bytes of loads; *bytes_read = that size):
+ * appended to a kernel inside a profiled range so the range's DRAM write bytes
+ * include the kernel's write-back */
+int gts_b200_l2_evict_read(void* stream, size_t* bytes_read);
+/* cudaProfilerStart / Stop: the profiled range of ncu --replay-mode range */
+int gts_b200_profiler_start(void);
+int gts_b200_profiler_stop(void);
 
 /* Halo exchange support for the horizontal decomposition:
  * copy the box [i0,i0+ni) x [j0,j0+nj) x [k0,k0+nk) (storage coordinates,

@@ -289,8 +289,9 @@ PREFETCH = 0  # gen_options pf_prefetch: stream rows loaded this many steps earl
 SWZ = False  # gen_options pf_swz: lane-alternating paired row loads (bank spreading)
 PDL = "off"  # gen_options pf_pdl: programmatic dependent launch off | early | late
 FRAME = False  # frame variant: the launch enumerates only the tiles outside an inner tile rectangle
+FASTDIV = True  # tile index division by multiply-high (gts_div_c) instead of the XU-pipe division
 DEFAULTS = {"pf_nw": 4, "pf_ri": 8, "pf_vj": 4, "pf_nbuf": 1, "pf_prefetch": 0, "pf_swz": 0, "pf_pdl": "off",
-            "pf_frame": 0}
+            "pf_frame": 0, "pf_fastdiv": 1}
 # Measured defaults per element size (profiles/sweep_hdiff_r1.md, hdiff
 # 256x256x80 on one B200, CUDA-graph timed):
 #  f64: 16x128 tiles, double-buffered TMA boxes: 16.9 us vs 18.1 us for
@@ -306,10 +307,13 @@ DEFAULTS = {"pf_nw": 4, "pf_ri": 8, "pf_vj": 4, "pf_nbuf": 1, "pf_prefetch": 0, 
 #       buffers all measured slower.
 #  f64 pf_pdl "late" (dependent launch triggered at each CTA's last tile): 16.14 ->
 #       15.97 us at 256^2, 6.13 -> 5.98 us at 128^2x64; f32 15.15 -> 15.22 (off).
+#  pf_fastdiv (tile index by multiply-high instead of the XU-pipe integer
+#       division; tools/abtest.py, medians of 7): f64 256^2 15.95 -> 15.79 us; f32
+#       15.12 -> 16.28 us (the f32 body schedules worse around it), so off for f32.
 GEOMETRY = {8: {"pf_nw": 2, "pf_ri": 4, "pf_vj": 4, "pf_nbuf": 2, "pf_prefetch": 1, "pf_swz": 1,
-                "pf_pdl": "late"},
+                "pf_pdl": "late", "pf_fastdiv": 1},
             4: {"pf_nw": 2, "pf_ri": 8, "pf_vj": 4, "pf_nbuf": 2, "pf_prefetch": 1, "pf_swz": 0,
-                "pf_pdl": "off"}}
+                "pf_pdl": "off", "pf_fastdiv": 0}}
 
 
 # Large binary64 domains use 4 warps per CTA: in eager launches 512x1024x80 runs
@@ -340,7 +344,7 @@ def configure(opts, esize: int = 0) -> None:
     fingerprint like the reference gen engine's tile options, gen.py:235-238).
     Unset options take the measured default of the group's smallest streamed
     element size ``esize`` (0: the generic DEFAULTS)."""
-    global NW, RI, VJ, TJ, TI, NBUF, PREFETCH, SWZ, PDL, FRAME
+    global NW, RI, VJ, TJ, TI, NBUF, PREFETCH, SWZ, PDL, FRAME, FASTDIV
     o = dict(DEFAULTS)
     o.update(GEOMETRY.get(esize, {}))
     o.update({k: v for k, v in (opts or {}).items() if k in DEFAULTS})
@@ -349,6 +353,7 @@ def configure(opts, esize: int = 0) -> None:
     SWZ = bool(int(o["pf_swz"]))
     PDL = str(o["pf_pdl"])
     FRAME = bool(int(o["pf_frame"]))
+    FASTDIV = bool(int(o["pf_fastdiv"]))
     TJ, TI = 32 * VJ, NW * RI
 
 
@@ -382,7 +387,7 @@ def emit(kname: str, plan, kplan, ctype: dict, dtypes: dict, opts=None):
       f"{[(x.name, x.rlo, x.rhi, x.clo, x.chi) for x in regw]}")
     minb = int((opts or {}).get("pf_minb", 0))  # min resident CTAs/SM (register cap), 0 = compiler's choice
     lb = f"{32 * NW}, {minb}" if minb else f"{32 * NW}"
-    frame_args = ", int fi0, int fi1, int fj0, int fj1" if FRAME else ""
+    frame_args = ", int fi0, int fi1, int fj0, int fj1" if FRAME else ", GtsFastDiv dvp, GtsFastDiv dvj"
     w(f"__global__ void __launch_bounds__({lb}) {kname}(const __grid_constant__ GtsParams p, {tm}, "
       f"int k0, int nkr, int tiles_i, int tiles_j, int ntiles{frame_args}) {{")
     w("  extern __shared__ __align__(1024) unsigned char smem[];")
@@ -406,10 +411,17 @@ def emit(kname: str, plan, kplan, ctype: dict, dtypes: dict, opts=None):
             w(f"{indent}int ti{sfx}, tj{sfx};")
             w(f"{indent}gts_frame_tile({tvar} % per{sfx}, tiles_j, fi0, fi1, fj0, fj1, ti{sfx}, tj{sfx});")
             w(f"{indent}const int i0{sfx} = ti{sfx} * {TI}, j0{sfx} = tj{sfx} * {TJ};")
-        else:
+        elif not FASTDIV:
             w(f"{indent}const int kk{sfx} = k0 + {tvar} / (tiles_i * tiles_j);")
             w(f"{indent}const int rem{sfx} = {tvar} % (tiles_i * tiles_j);")
             w(f"{indent}const int i0{sfx} = (rem{sfx} / tiles_j) * {TI}, j0{sfx} = (rem{sfx} % tiles_j) * {TJ};")
+        else:
+            # tile index -> (plane, row, column) by multiply-high division (no XU)
+            w(f"{indent}const int q{sfx} = gts_div_c({tvar}, dvp);")
+            w(f"{indent}const int kk{sfx} = k0 + q{sfx};")
+            w(f"{indent}const int rem{sfx} = {tvar} - q{sfx} * (tiles_i * tiles_j);")
+            w(f"{indent}const int r{sfx}_ = gts_div_c(rem{sfx}, dvj);")
+            w(f"{indent}const int i0{sfx} = r{sfx}_ * {TI}, j0{sfx} = (rem{sfx} - r{sfx}_ * tiles_j) * {TJ};")
 
     def issue(tvar, buf):
         w(f"    {{ const int tt = {tvar};")
@@ -658,7 +670,7 @@ def emit(kname: str, plan, kplan, ctype: dict, dtypes: dict, opts=None):
             "      if (nkr > 0) {",
             "        const int ntiles = tiles_i * tiles_j * nkr;",
         ]
-        targs = f"{tm_args}, k0, nkr, tiles_i, tiles_j, ntiles"
+        targs = f"{tm_args}, k0, nkr, tiles_i, tiles_j, ntiles, gts_fastdiv(tiles_i * tiles_j), gts_fastdiv(tiles_j)"
     launch = [
         "    {",
         f"      const int k0 = {_bound(kplan.interval.start)}, k1 = {_bound(kplan.interval.end)};",

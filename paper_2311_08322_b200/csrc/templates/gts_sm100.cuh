@@ -179,6 +179,31 @@ __device__ __forceinline__ void gts_tmem_store_f32(uint32_t taddr, float v) {
 }
 
 // ---------------------------------------------------------------------------
+// Division by a launch-constant divisor without the XU pipe: n / d as a
+// multiply-high and a shift (Granlund-Montgomery round-up method, exact for
+// 0 <= n < 2^31, 1 <= d < 2^31).  A 32-bit integer division otherwise
+// expands to I2F + MUFU.RCP + F2I on the XU pipe -- the pipe that also
+// carries every binary32 <-> binary64 conversion, which bounds the f32-storage
+// tile kernel (ncu: XU 66 % active).
+// ---------------------------------------------------------------------------
+struct GtsFastDiv {
+  uint32_t d, m, s;
+};
+static inline GtsFastDiv gts_fastdiv(int d) {
+  GtsFastDiv f;
+  f.d = (uint32_t)(d > 0 ? d : 1);
+  uint32_t l = 0;
+  while ((1u << l) < f.d) ++l;  // ceil(log2 d)
+  const uint32_t p = 31 + l;
+  f.m = (uint32_t)(((1ull << p) + f.d - 1) / f.d);
+  f.s = p - 32;
+  return f;
+}
+__device__ __forceinline__ int gts_div_c(int n, const GtsFastDiv& f) {
+  return f.d == 1 ? n : (int)(__umulhi((uint32_t)n, f.m) >> f.s);
+}
+
+// ---------------------------------------------------------------------------
 // Frame tiles: the tiles of a tiles_i x tiles_j plane outside the inner
 // rectangle [fi0, fi1) x [fj0, fj1), enumerated row by row (the frame launch
 // of a decomposed step: top rows, then the left / right tiles of the middle

@@ -54,6 +54,9 @@ SIGNATURES = {
     "gts_b200_flags_wait_next": (_INT, [_VP, _VP, _INT, _VP]),
     "gts_b200_event_elapsed_ms": (_INT, [_c.POINTER(_c.c_float), _VP, _VP]),
     "gts_b200_l2_flush": (_INT, [_VP]),
+    "gts_b200_l2_evict_read": (_INT, [_VP, _c.POINTER(_SZ)]),
+    "gts_b200_profiler_start": (_INT, []),
+    "gts_b200_profiler_stop": (_INT, []),
     "gts_b200_pack_box": (_INT, [_VP, _VP] + [_I64] * 9 + [_INT, _VP]),
     "gts_b200_unpack_box": (_INT, [_VP, _VP] + [_I64] * 9 + [_INT, _VP]),
     "gts_b200_memcpy2d_h2d": (_INT, [_VP, _SZ, _VP, _SZ, _SZ, _SZ, _VP]),

@@ -4,8 +4,10 @@
 
 Writes profiles/ncu_<round>.md (key metrics + top stalls per captured kernel,
 launch-list shares) and profiles/ncu_traffic.json (DRAM bytes per launch, read
-+ write, from the --set full captures; bench.py reports them as
-roofline.traffic).
++ write; bench.py reports them as roofline.traffic).  The traffic comes from
+the range-replay captures of tools/ncu_traffic.py (the launch followed by a
+read-only L2 eviction, so the write-back is counted) when present, else from
+the --set full captures (cold reads, but the writes still in L2 are missed).
 """
 import csv
 import io
@@ -28,10 +30,31 @@ def raw(path):
     return rows[0], rows[1], rows[2:]
 
 
+def range_traffic(wl):
+    """Read + write DRAM bytes of one launch from tools/ncu_traffic.py's
+    range replay (launch + read-only eviction; reads minus the eviction)."""
+    c, j = OUT / f"traffic_{wl}.csv", OUT / f"traffic_{wl}.json"
+    if not (c.exists() and j.exists()):
+        return None
+    rows = [x for x in csv.reader(io.StringIO(c.read_text())) if len(x) > 12 and x[0] != "ID"]
+    m = {x[10]: float(x[12].replace(",", "")) for x in rows}
+    if "dram__bytes_read.sum" not in m:
+        return None
+    meta = json.loads([ln for ln in j.read_text().splitlines() if ln.startswith("{")][0])
+    rd = m["dram__bytes_read.sum"] - meta["evict_read_bytes"]
+    wr = m["dram__bytes_write.sum"]
+    return {"dram_read_mb": rd / 1e6, "dram_write_mb": wr / 1e6, "traffic_bytes": rd + wr,
+            "algorithmic_bytes": meta["algorithmic_bytes"],
+            "traffic_over_algorithmic": round((rd + wr) / meta["algorithmic_bytes"], 3),
+            "source": f"traffic_{wl}.csv: ncu --replay-mode range over [launch, gts_b200_l2_evict_read] "
+                      f"(tools/ncu_traffic.py); reads minus the eviction's {meta['evict_read_bytes']} B"}
+
+
 def main(r):
     md = [f"# ncu summaries, round {r}", "",
           "Captured on one B200 with `profiles/capture.sh " + r + "` (ncu --set full, --clock-control none,",
-          "caches flushed between replays, so DRAM bytes are cold-cache per launch).", ""]
+          "caches flushed between replays, so DRAM bytes are cold-cache per launch).  The traffic lines come",
+          "from the range replays of tools/ncu_traffic.py, which include the write-back.", ""]
     traffic = {}
     for wl, pat in CAPTURES.items():
         rep = OUT / (pat.format(r=r) + ".ncu-rep")
@@ -63,7 +86,15 @@ def main(r):
         rd, wr = mb("dram__bytes_read.sum"), mb("dram__bytes_write.sum")
         traffic[wl] = {"dram_read_mb": rd, "dram_write_mb": wr, "traffic_bytes": (rd + wr) * 1e6,
                        "duration_us": float(row[hdr.index("gpu__time_duration.sum")]),
-                       "source": rep.name}
+                       "source": rep.name + " (kernel replay: writes still in L2 not counted)"}
+        rr = range_traffic(wl)
+        if rr is not None:
+            traffic[wl] = rr
+        t = traffic[wl]
+        md += [f"DRAM traffic per launch incl. write-back: read {t['dram_read_mb']:.1f} MB + write "
+               f"{t['dram_write_mb']:.1f} MB = {t['traffic_bytes'] / 1e6:.1f} MB"
+               + (f" ({t['traffic_over_algorithmic']:.3f}x the algorithmic {t['algorithmic_bytes'] / 1e6:.1f} MB)"
+                  if "algorithmic_bytes" in t else ""), ""]
     lst = OUT / f"launches_{r}.csv"
     if lst.exists():
         lines = [ln for ln in lst.read_text().splitlines() if ln.startswith('"')]
