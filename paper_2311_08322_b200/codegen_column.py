@@ -617,16 +617,26 @@ def _emit_variant(kname, plan, sp: ThomasSpec, v: Variant, ctype, dtypes, opts):
             w(f"{indent}}}")
 
     def prologue_rd(ring: bool):
+        # dj may be a C expression (a warp-edge lane's per-lane column)
         if ring:
             def rd(name, di, dj):
                 hb = v.hbox[name]
-                return f"uh_{name}[kk * {(rows + hb.rows_extra) * hb.cols} + {di * hb.cols + dj}]"
+                off = di * hb.cols + dj if isinstance(dj, int) else f"{di * hb.cols} + {dj}"
+                return f"uh_{name}[kk * {(rows + hb.rows_extra) * hb.cols} + {off}]"
         else:
             def rd(name, di, dj):
                 ii = f"(ic{di:+d})" if di else "ic"
-                jj = f"(jc{dj:+d})" if dj else "jc"
+                jj = (f"(jc{dj:+d})" if dj else "jc") if isinstance(dj, int) else f"(jc + {dj})"
                 return f"GTS_AT(p.f_{name}, {ii}, {jj}, k)"
         return rd
+
+    # neighbour-lane shuffles in the prologue (codegen_prologue.lane_shuffled):
+    # consumer lanes are 32 consecutive j columns of one i row.  Bitwise, but
+    # measured slower (tools/abtest.py, dycore 512^2x80, medians of 3: 190.5 vs
+    # 172.8 us/step: the edge evaluation's per-lane column defeats the
+    # compiler's sharing of the cross's loads and the body grows from 3816 to
+    # 4656 instructions), so it is opt-in
+    pro_lane = "lane" if (opts or {}).get("pro_shfl", False) else None
 
     pro_batch = sp.pro is not None and (opts or {}).get("pro_batch", True)
 
@@ -675,7 +685,7 @@ def _emit_variant(kname, plan, sp: ThomasSpec, v: Variant, ctype, dtypes, opts):
         w(f"{indent}#pragma unroll")
         w(f"{indent}for (int kk = 0; kk < {KB}; ++kk) {{")
         vals = codegen_prologue.emit_point(sp.pro, prologue_rd(True), ctype, out, indent + "  ",
-                                           mat_read=mat_reads())
+                                           mat_read=mat_reads(), lane=pro_lane)
         for f, var in vals.items():
             w(f"{indent}  pv_{f}[kk] = {var};")
         w(f"{indent}}}")
@@ -691,7 +701,11 @@ def _emit_variant(kname, plan, sp: ThomasSpec, v: Variant, ctype, dtypes, opts):
         elif sp.pro is not None:
             # the fused PARALLEL prologue at this thread's (i, j, k)
             w(f"{indent}// fused prologue ({', '.join(sp.pro.exports)})")
-            ctx.pro_vals = codegen_prologue.emit_point(sp.pro, prologue_rd(ctx.ring), ctype, out, indent)
+            # the exact-division replay reads global memory at clamped columns:
+            # a lane past the domain's edge would hand its neighbour the wrong
+            # value, so only ring reads (box columns = lane columns) shuffle
+            ctx.pro_vals = codegen_prologue.emit_point(sp.pro, prologue_rd(ctx.ring), ctype, out, indent,
+                                                       lane=pro_lane if ctx.ring else None)
         groups = [gf[group]] if group is not None else gf
         for gi, (iv, stages) in enumerate(groups):
             if group is None:

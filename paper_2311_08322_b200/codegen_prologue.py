@@ -184,21 +184,28 @@ def _vn(name: str, oi: int, oj: int) -> str:
 
 
 class _PointCtx:
-    """Reads of one stage evaluated at horizontal offset (oi, oj)."""
+    """Reads of one stage evaluated at horizontal offset (oi, oj); ``oj`` may
+    be a C expression (the per-lane column of a warp-edge evaluation, which
+    reads only the group's inputs)."""
 
-    def __init__(self, ps: PrologueSpec, read_input, oi: int, oj: int, mat_read=None):
+    def __init__(self, ps: PrologueSpec, read_input, oi: int, oj, mat_read=None):
         self.ps, self.read_input, self.oi, self.oj = ps, read_input, oi, oj
         self.pool = None
         self.rename = {}
         self.mat_read = mat_read or {}
 
+    def _col(self, dj):
+        if isinstance(self.oj, str):
+            return f"({self.oj}{dj:+d})" if dj else self.oj
+        return self.oj + dj
+
     def read(self, name, off):
         di, dj, _ = off
         if name in self.mat_read:
-            return f"((double){self.mat_read[name](self.oi + di, self.oj + dj)})"
+            return f"((double){self.mat_read[name](self.oi + di, self._col(dj))})"
         if name in self.ps.required:
-            return _vn(name, self.oi + di, self.oj + dj)
-        return f"((double){self.read_input(name, self.oi + di, self.oj + dj)})"
+            return _vn(name, self.oi + di, self._col(dj))
+        return f"((double){self.read_input(name, self.oi + di, self._col(dj))})"
 
     def target(self, name):
         return self.rename.get(name) or _vn(name, self.oi, self.oj)
@@ -223,27 +230,66 @@ def _emit_stmt(stmt, ctx, ctype: dict, out: list, indent: str) -> None:
     raise TypeError(type(stmt).__name__)
 
 
+def lane_shuffled(ps: PrologueSpec, st) -> list:
+    """Rows ``oi`` at which stage ``st`` is needed at (oi, -1), (oi, 0) AND
+    (oi, +1) and reads only the group's inputs (hdiff's ``lap`` on the 5-point
+    cross: oi = 0).  With one warp lane per consecutive j column, lane l's
+    value at (oi, -1) is lane l-1's at (oi, 0) -- the same instructions on the
+    same inputs, so bitwise equal -- and only the two warp-edge lanes need a
+    real evaluation: one per-lane evaluation at column ``ex_`` (-1 on lane 0,
+    +1 elsewhere) replaces two."""
+    if any(a.field in ps.required for a in reads(st.body)):
+        return []
+    offs = set()
+    for g in writes(st.body):
+        offs |= set(ps.required[g])
+    return sorted(oi for (oi, oj) in offs if oj == 0 and (oi, -1) in offs and (oi, 1) in offs)
+
+
 def emit_point(ps: PrologueSpec, read_input, ctype: dict, out: list, indent: str,
-               mat_read=None) -> dict:
+               mat_read=None, lane: str = None) -> dict:
     """Straight-line evaluation of the group at the thread's own point.
     ``read_input(name, di, dj)`` spells a read of an input at a horizontal
-    offset; ``mat_read`` {temp: f(di, dj)} spells reads of temporaries
-    already materialized in shared memory (their stages are skipped).
-    Returns {export: C variable holding its value}."""
+    offset (``dj`` may be a C expression); ``mat_read`` {temp: f(di, dj)}
+    spells reads of temporaries already materialized in shared memory (their
+    stages are skipped).  ``lane``: the C lane index when the warp's 32 lanes
+    are 32 consecutive j columns -- enables the neighbour-lane shuffles of
+    ``lane_shuffled``.  Returns {export: C variable holding its value}."""
     mat_read = mat_read or {}
     for f, offs in sorted(ps.required.items()):
         if f in mat_read:
             continue
         for (oi, oj) in offs:
             out.append(f"{indent}double {_vn(f, oi, oj)};")
+    edge_decl = False
     for st in ps.stages:
         if writes(st.body) & set(mat_read):
             continue
         offs = set()
         for g in writes(st.body):
             offs |= set(ps.required[g])
+        shfl = lane_shuffled(ps, st) if lane is not None else []
         for (oi, oj) in sorted(offs):
+            if oi in shfl and oj in (-1, 1):
+                continue
             _emit_stmt(st.body, _PointCtx(ps, read_input, oi, oj, mat_read), ctype, out, indent)
+        for oi in shfl:
+            if not edge_decl:
+                out.append(f"{indent}const int ex_ = ({lane}) == 0 ? -1 : 1;  // warp-edge column")
+                edge_decl = True
+            ctx = _PointCtx(ps, read_input, oi, "ex_", mat_read)
+            ctx.rename = {g: f"pe_{g}_{_vn(g, oi, 0)[3:]}" for g in writes(st.body)}
+            for g in writes(st.body):
+                out.append(f"{indent}double {ctx.rename[g]};")
+            _emit_stmt(st.body, ctx, ctype, out, indent)
+            for g in writes(st.body):
+                own, e = _vn(g, oi, 0), ctx.rename[g]
+                # every lane executes both shuffles (full-mask convergence);
+                # only the selection depends on the lane
+                out.append(f"{indent}const double su_{own} = __shfl_up_sync(0xffffffffu, {own}, 1);")
+                out.append(f"{indent}const double sd_{own} = __shfl_down_sync(0xffffffffu, {own}, 1);")
+                out.append(f"{indent}{_vn(g, oi, -1)} = ({lane}) == 0 ? {e} : su_{own};")
+                out.append(f"{indent}{_vn(g, oi, 1)} = ({lane}) == 31 ? {e} : sd_{own};")
     return {f: _vn(f, 0, 0) for f in ps.exports}
 
 

@@ -77,6 +77,7 @@ def test_dycore_timeloop_graph_matches_oracle(gpu):
     ({"fuse_prologue": False}, 128),  # hdiff launch + TMEM column kernel streaming uh
     ({"tmem": False}, 128),           # hdiff launch + generic column kernel
     ({"pro_coop": True}, 128),        # cooperative shared-memory Laplacian (opt-in)
+    ({"pro_shfl": True}, 128),        # neighbour-lane shuffles of the Laplacian (opt-in)
     ({}, 8),                          # TMA-incompatible storages: run-time fallback chain
 ])
 def test_dycore_launch_paths_match_golden(gpu, opts, align):
