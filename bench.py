@@ -572,7 +572,9 @@ def c4_weak_scaling(dist, args, tile=(512, 1024, 80)):
     ms_s, _, _, lps_s = decomposed_hdiff(dist, nst, args.warmup, tile=tile, transport="none", split=True)
     out["split_us"] = ms_s * 1e3
     out["split_launches_per_step"] = lps_s
-    transports = ("nccl", "peer") if dist.world > 1 and not dist.shared else ()
+    # (ranks sharing one GPU -- GTS_BENCH_SHARED_GPU -- exercise the peer
+    # transport only: NCCL cannot put two ranks on one device)
+    transports = (("peer",) if dist.shared else ("nccl", "peer")) if dist.world > 1 else ()
     for tr in transports:
         try:
             ms, gdom, grid, lps = decomposed_hdiff(dist, nst, args.warmup, tile=tile, transport=tr)
