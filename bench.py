@@ -511,8 +511,10 @@ def decomposed_hdiff(dist, steps, warmup, tile=(512, 1024, 80), transport="nccl"
     tile per GPU (weak scaling; 2048x2048x80 at 8 GPUs on a 4x2 grid).  Each
     step = the halo exchange of inp (``nccl``: NCCL send/recv; ``peer``: CUDA
     IPC peer stores + flags) overlapped with the interior, then the boundary
-    frame (decomp.DecomposedStep: 2 launches per step); ``none``: the tile
-    alone, as at N=1.  The timed steps are replayed from one CUDA graph (the
+    frame (decomp.DecomposedStep: 2 launches per step); ``fused``: a ping-pong
+    loop whose tile kernel stores its boundary output straight into the
+    neighbours' halos (decomp.PeerFusedStep: 1 launch per step); ``none``: the
+    tile alone, as at N=1.  The timed steps are replayed from one CUDA graph (the
     NCCL calls are captured too).  Returns (max-over-ranks ms per step,
     global domain, grid, launches per step)."""
     import paper_2311_08322_b200 as b200
@@ -522,9 +524,27 @@ def decomposed_hdiff(dist, steps, warmup, tile=(512, 1024, 80), transport="nccl"
     gdom = (tile[0] * grid[0], tile[1] * grid[1], tile[2])
     d = decomp.Decomposition(gdom, grid, dist.rank if transport != "none" else 0)
     ldom = d.local_domain
-    st = b200.compile_stencil(workloads.source("hdiff"), "hdiff")
     rng = np.random.default_rng(1000 + dist.rank)
-    inp = b200.from_array(rng.uniform(-1, 1, (ldom[0] + 4, ldom[1] + 4, ldom[2])), (2, 2, 0))
+    vals = rng.uniform(-1, 1, (ldom[0] + 4, ldom[1] + 4, ldom[2]))
+    if transport == "fused":
+        # hdiff as a ping-pong time loop (out is the next step's inp) with the
+        # halo exchange fused into the tile kernel: its output stores also go
+        # into the neighbours' halos (peer memory), one launch per step
+        st = b200.compile_stencil(workloads.source("hdiff"), "hdiff", gen_options={"mirror": "out"})
+        A, B = b200.from_array(vals, (2, 2, 0)), b200.from_array(vals, (2, 2, 0))
+        step = decomp.PeerFusedStep(st, d, [{"inp": A, "out": B}, {"inp": B, "out": A}], {"coeff": 0.05},
+                                    "out", (2, 2))
+        for _ in range(2 * max(1, warmup // 2)):
+            step()
+        native.synchronize(step.stream)
+        module = st.build_info["module"]
+        steps += steps % 2
+        n0 = module.launch_count()
+        replay = step.graph(steps)
+        lps = (module.launch_count() - n0) / steps
+        return _time_replay(dist, replay, step.stream, steps, step), gdom, grid, lps
+    st = b200.compile_stencil(workloads.source("hdiff"), "hdiff")
+    inp = b200.from_array(vals, (2, 2, 0))
     out = b200.allocate("f64", ldom)
     if transport == "peer":
         step = decomp.PeerDecomposedStep(st, d, {"inp": inp, "out": out}, {"coeff": 0.05}, "inp", (2, 2))
@@ -539,6 +559,14 @@ def decomposed_hdiff(dist, steps, warmup, tile=(512, 1024, 80), transport="nccl"
     n0 = module.launch_count()
     replay = step.graph(steps)
     lps = (module.launch_count() - n0) / steps
+    return _time_replay(dist, replay, stream, steps, step), gdom, grid, lps
+
+
+def _time_replay(dist, replay, stream, steps, step) -> float:
+    """One warm replay, then one timed replay of ``steps`` steps (CUDA
+    events on the step's stream, max over ranks): ms per step."""
+    from paper_2311_08322_b200 import native
+
     replay.launch()  # upload + warm replay
     native.synchronize(stream)
     e0, e1 = native.Event(), native.Event()
@@ -552,7 +580,7 @@ def decomposed_hdiff(dist, steps, warmup, tile=(512, 1024, 80), transport="nccl"
     ms = dist.max(e0.elapsed_ms(e1) / steps)
     if hasattr(step, "close"):
         step.close()
-    return ms, gdom, grid, lps
+    return ms
 
 
 def c4_weak_scaling(dist, args, tile=(512, 1024, 80)):
@@ -573,8 +601,11 @@ def c4_weak_scaling(dist, args, tile=(512, 1024, 80)):
     out["split_us"] = ms_s * 1e3
     out["split_launches_per_step"] = lps_s
     # (ranks sharing one GPU -- GTS_BENCH_SHARED_GPU -- exercise the peer
-    # transport only: NCCL cannot put two ranks on one device)
-    transports = (("peer",) if dist.shared else ("nccl", "peer")) if dist.world > 1 else ()
+    # transports only: NCCL cannot put two ranks on one device)
+    transports = (("peer", "fused") if dist.shared else ("nccl", "peer", "fused")) if dist.world > 1 else ()
+    if dist.world == 1:  # the fused step's kernel (mirror build, no neighbours) as one launch
+        ms_f, _, _, lps_f = decomposed_hdiff(dist, nst, args.warmup, tile=tile, transport="fused")
+        out["fused_us"] = ms_f * 1e3
     for tr in transports:
         try:
             ms, gdom, grid, lps = decomposed_hdiff(dist, nst, args.warmup, tile=tile, transport=tr)

@@ -317,6 +317,16 @@ def make_diagonally_dominant(rng: np.random.Generator, shape):
 # ---------------------------------------------------------------------------
 
 
+def hdiff_run(u: np.ndarray, steps: int, coeff: float = 0.05) -> np.ndarray:
+    """``steps`` hdiff steps as a ping-pong time loop (out becomes the next
+    step's inp; the 2-cell halo keeps its initial values: Dirichlet), the C
+    restatement per step."""
+    u = np.array(u, copy=True)
+    for _ in range(steps):
+        u[2:-2, 2:-2, :] = hdiff_c(u, coeff)
+    return u
+
+
 def dycore_update_np(x: np.ndarray, tau: float) -> np.ndarray:
     """The interval-specialised update of dycore.gts (last computation):
     [0,1) and [K-1,K): u_out = x; [1,K-1): u_out = x + tau*((x[k+1] - 2*x) + x[k-1])

@@ -494,19 +494,21 @@ def mirror_setter_name(impl, fp) -> str:
 
 
 def _mirror_field(plan: Plan, opts: dict):
-    """gen_options ``mirror``: the api output field whose stores the column
-    template also sends into neighbour halos (decomp.PeerFusedStep).  Only
-    a field written by exactly one column kernel (the TMEM template, whose
-    launch refuses to fall back) can be mirrored."""
+    """gen_options ``mirror``: the api output field whose stores the producing
+    kernel also sends into neighbour halos (decomp.PeerFusedStep).  Only a
+    field written by exactly one launch can be mirrored: a TMEM column kernel
+    or a fused PARALLEL tile kernel (both store it once per point from
+    registers; their launches refuse to fall back to templates without the
+    mirror stores)."""
     m = opts.get("mirror")
     if not m:
         return None
     if m not in {f.name for f in plan.impl.api_fields}:
         raise ValueError(f"gen_options mirror: '{m}' is not an api field")
     writers = [k for k in plan.kernels if any(m in writes(r.stage.body) for r in k.stages)]
-    if len(writers) != 1 or writers[0].kind != "column":
-        raise ValueError(f"gen_options mirror: '{m}' must be written by exactly one column kernel "
-                         f"(plan {' '.join(plan.describe())})")
+    if len(writers) != 1 or writers[0].kind not in ("column", "pfused"):
+        raise ValueError(f"gen_options mirror: '{m}' must be written by exactly one column or fused "
+                         f"PARALLEL kernel (plan {' '.join(plan.describe())})")
     return m
 
 
@@ -655,6 +657,11 @@ def _generate_source(plan: Plan, fp, options: Optional[dict] = None) -> str:
                 nm = f"{kname}_s{r.idx}"
                 out.extend(_point_kernel(nm, r.stage, ctype, dtypes))
                 fb += pstage_launch(nm, r.stage)
+            if mirror and any(mirror in writes(r.stage.body) for r in k.stages):
+                # the mirrored field's stores exist only in the tile template
+                if res is None:
+                    raise ValueError(f"gen_options mirror: '{mirror}' needs the fused PARALLEL tile template")
+                fb = [f"  return {GTS_ERR_UNSUPPORTED};  // mirrored field: no fallback without the mirror stores"]
             if res is None:
                 launches += fb
                 for t in k.local_temps:

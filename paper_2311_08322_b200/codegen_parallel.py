@@ -290,6 +290,7 @@ SWZ = False  # gen_options pf_swz: lane-alternating paired row loads (bank sprea
 PDL = "off"  # gen_options pf_pdl: programmatic dependent launch off | early | late
 FRAME = False  # frame variant: the launch enumerates only the tiles outside an inner tile rectangle
 FASTDIV = True  # tile index division by multiply-high (gts_div_c) instead of the XU-pipe division
+MIRROR = None  # gen_options mirror: the buffered api output also stored into neighbour halo boxes
 DEFAULTS = {"pf_nw": 4, "pf_ri": 8, "pf_vj": 4, "pf_nbuf": 1, "pf_prefetch": 0, "pf_swz": 0, "pf_pdl": "off",
             "pf_frame": 0, "pf_fastdiv": 1}
 # Measured defaults per element size (profiles/sweep_hdiff_r1.md, hdiff
@@ -365,12 +366,17 @@ def _min_esize(plan, kplan, dtypes: dict) -> int:
 
 
 def emit(kname: str, plan, kplan, ctype: dict, dtypes: dict, opts=None):
-    global _LAST_ESIZE
+    global _LAST_ESIZE, MIRROR
     _LAST_ESIZE = _min_esize(plan, kplan, dtypes)
     configure(opts, _LAST_ESIZE)
     geo = eligible(plan, kplan, dtypes)
     if geo is None:
         return None
+    MIRROR = (opts or {}).get("mirror") or None
+    if MIRROR and not any(MIRROR in writes(st.body) for st in geo.stages):
+        MIRROR = None  # another launch of the plan writes it
+    if MIRROR and MIRROR not in geo.buffered:
+        return None  # a mirrored output must be stored from registers once per point
     impl = plan.impl
     api = {f.name for f in impl.api_fields}
     local = set(kplan.local_temps)
@@ -458,8 +464,31 @@ def emit(kname: str, plan, kplan, ctype: dict, dtypes: dict, opts=None):
     w("    gts_mbar_wait(&full[buf], ph);")
     w("    const unsigned char* sb = smem + buf * " + str(geo.buf_bytes) + ";")
     tile_coords("t", "", "    ")
+
     w(f"    const int jl = j0 + lane * {VJ};")
     w(f"    const int ra = i0 + warp * {RI};")
+    if MIRROR in geo.buffered:
+        # the mirror boxes (gen_options mirror) this tile intersects, uniform per
+        # CTA: up to 3 (a face in i, a face in j, their corner) are kept in
+        # registers -- target plane pointer, row range, this lane's column mask
+        # -- so a boundary row costs a few predicated stores; more (a tile
+        # spanning the whole domain) take the general loop
+        t_ = ctype[MIRROR]
+        w("    int nmir_ = 0;")
+        w(f"    {t_}* mbp_[3] = {{nullptr, nullptr, nullptr}};")
+        w("    long long msi_[3] = {0, 0, 0}, msj_[3] = {0, 0, 0};")
+        w("    int mi0_[3] = {0, 0, 0}, mi1_[3] = {0, 0, 0};")
+        w("    unsigned mcm_[3] = {0u, 0u, 0u};")
+        w("    for (int d = 0; d < p.mir.n; ++d) {")
+        w(f"      if (!(i0 < p.mir.i1[d] && i0 + {TI} > p.mir.i0[d] && j0 < p.mir.j1[d] && j0 + {TJ} > p.mir.j0[d])) continue;")
+        w("      unsigned cm = 0u;")
+        w(f"      for (int q = 0; q < {VJ}; ++q) {{ const int c = jl + q; if (c < nj && c >= p.mir.j0[d] && c < p.mir.j1[d]) cm |= 1u << q; }}")
+        for m in range(3):  # static slots (a runtime index would put the arrays in local memory)
+            w(f"      {'if' if m == 0 else 'else if'} (nmir_ == {m}) {{ mbp_[{m}] = p.mir.base[d] + (long long)kk * p.mir.sk[d]; "
+              f"msi_[{m}] = p.mir.si[d]; msj_[{m}] = p.mir.sj[d]; mi0_[{m}] = p.mir.i0[d]; mi1_[{m}] = p.mir.i1[d]; "
+              f"mcm_[{m}] = cm; }}")
+        w("      ++nmir_;")
+        w("    }")
     # per-column store validity
     for c in range(VJ):
         w(f"    const bool okc_{c} = (jl + {c}) < nj;")
@@ -616,17 +645,44 @@ def emit(kname: str, plan, kplan, ctype: dict, dtypes: dict, opts=None):
                 e = 8 if dtypes[f] == ir.F64 else 4
                 w(f"      if (r < ni{' && nkr < 0' if pf_debug == 'nostore' else ''}) {{")
                 w(f"        {ctype[f]}* const op = &GTS_AT(p.f_{f}, r, jl, kk);")
-                w(f"        if (jl + {VJ} <= nj && p.f_{f}.sj == 1 && (((uintptr_t)op) & 15) == 0) {{")
-                if e == 8:
-                    for q in range(0, VJ, 2):
-                        w(f"          *reinterpret_cast<double2*>(op + {q}) = make_double2(o_{f}[{q}], o_{f}[{q + 1}]);")
-                else:
-                    for q in range(0, VJ, 4):
-                        w(f"          *reinterpret_cast<float4*>(op + {q}) = make_float4(o_{f}[{q}], o_{f}[{q + 1}], o_{f}[{q + 2}], o_{f}[{q + 3}]);")
-                w("        } else {")
+                vec = 16 // e  # elements per 16-B vector store
+                if VJ % vec == 0:
+                    w(f"        if (jl + {VJ} <= nj && p.f_{f}.sj == 1 && (((uintptr_t)op) & 15) == 0) {{")
+                    if e == 8:
+                        for q in range(0, VJ, 2):
+                            w(f"          *reinterpret_cast<double2*>(op + {q}) = make_double2(o_{f}[{q}], o_{f}[{q + 1}]);")
+                    else:
+                        for q in range(0, VJ, 4):
+                            w(f"          *reinterpret_cast<float4*>(op + {q}) = make_float4(o_{f}[{q}], o_{f}[{q + 1}], o_{f}[{q + 2}], o_{f}[{q + 3}]);")
+                    w("        } else {")
+                else:  # fewer columns per lane than one vector (the frame variant): scalar stores
+                    w("        {")
                 for q in range(VJ):
                     w(f"          if (jl + {q} < nj) op[(long long){q} * p.f_{f}.sj] = o_{f}[{q}];")
                 w("        }")
+                if f == MIRROR:
+                    # gen_options mirror: the row's values inside a neighbour's halo
+                    # box also go there (peer stores; boundary tiles only)
+                    w("        if (nmir_ > 0) {")
+                    w("          if (nmir_ <= 3) {")
+                    w("            #pragma unroll")
+                    w("            for (int m = 0; m < 3; ++m) {")
+                    w("              if (m < nmir_ && r >= mi0_[m] && r < mi1_[m] && mcm_[m]) {")
+                    w(f"                {ctype[f]}* const mb_ = mbp_[m] + (long long)r * msi_[m];")
+                    for q in range(VJ):
+                        w(f"                if (mcm_[m] & {1 << q}u) mb_[(long long)(jl + {q}) * msj_[m]] = o_{f}[{q}];")
+                    w("              }")
+                    w("            }")
+                    w("          } else {")
+                    w("            for (int d = 0; d < p.mir.n; ++d) {")
+                    w("              if (r < p.mir.i0[d] || r >= p.mir.i1[d]) continue;")
+                    w(f"              {ctype[f]}* const mb_ = p.mir.base[d] + (long long)r * p.mir.si[d] + (long long)kk * p.mir.sk[d];")
+                    for q in range(VJ):
+                        w(f"              if (jl + {q} < nj && jl + {q} >= p.mir.j0[d] && jl + {q} < p.mir.j1[d]) "
+                          f"mb_[(long long)(jl + {q}) * p.mir.sj[d]] = o_{f}[{q}];")
+                    w("            }")
+                    w("          }")
+                    w("        }")
                 w("      }")
         w("    }")
     w("    __syncthreads();  // both buffers' readers done before the next prefetch reuses this one")

@@ -251,23 +251,34 @@ def test_mirror_boxes_cover_every_halo_once(grid):
 
 
 def test_mirror_option_rejects_unsupported_fields():
-    """gen_options mirror needs an api field written by one column kernel."""
+    """gen_options mirror needs an api field written by one TMEM column or
+    fused PARALLEL tile kernel (the templates that carry the mirror stores):
+    a temporary, or an output only a per-point fallback kernel can produce
+    (a vertical-offset read), is refused at build time; hdiff's out is
+    accepted."""
     import paper_2311_08322_b200 as b200
     from paper_2311_08322_b200 import workloads
 
-    for src, name, field in ((workloads.source("hdiff"), "hdiff", "out"),
-                             (workloads.source("dycore"), "dycore", "lap")):
+    vshift = ("stencil vshift(inp: Field[f64], out: Field[f64]):\n"
+              "    with computation(PARALLEL):\n"
+              "        with interval(0, -1):\n"
+              "            out = inp[0, 0, 1]\n")
+    for src, name, field in ((workloads.source("dycore"), "dycore", "lap"), (vshift, "vshift", "out")):
         with pytest.raises(Exception, match="mirror"):
             b200.compile_stencil(src, name, gen_options={"mirror": field})
+    st = b200.compile_stencil(workloads.source("hdiff"), "hdiff", gen_options={"mirror": "out"})
+    assert st.build_info["module"]._mirror_fn is not None
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("kernel", ["dycore", "hdiff"])
 @pytest.mark.parametrize("nproc,steps", [(2, 4), (4, 2)])
-def test_peer_fused_dycore_multiprocess(nproc, steps):
-    """The dycore step with the halo exchange fused into the producing
-    kernel (PeerFusedStep, peer stores from the column kernel's epilogue,
-    corners included): bitwise the undecomposed oracle, eager and replayed
-    from a CUDA graph, with 2 and 4 processes sharing one B200."""
+def test_peer_fused_multiprocess(nproc, steps, kernel):
+    """A time loop with the halo exchange fused into the producing kernel
+    (PeerFusedStep, peer stores corners included): the dycore (TMEM column
+    kernel's epilogue) and the hdiff ping-pong loop (fused PARALLEL tile
+    kernel's output stores); bitwise the undecomposed oracle, eager and
+    replayed from a CUDA graph, with 2 and 4 processes sharing one B200."""
     import subprocess
     import sys
     from pathlib import Path
@@ -275,7 +286,7 @@ def test_peer_fused_dycore_multiprocess(nproc, steps):
     repo = Path(__file__).resolve().parent.parent
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
-           str(repo / "tools" / "peer_fused_check.py"), str(steps)]
+           str(repo / "tools" / "peer_fused_check.py"), str(steps), "--kernel", kernel]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=400, cwd=str(repo))
     assert r.returncode == 0 and r.stdout.count("FUSED_PEER_OK") == nproc, (r.stdout[-2000:], r.stderr[-3000:])
 
@@ -480,3 +491,53 @@ def test_interior_plus_frame_launch_bitwise(dom):
         # interior points are either untouched (poison) or the same values
         inner = got[~band]
         assert np.all(np.isnan(inner) | (inner == want[~band]))
+
+
+@pytest.mark.gpu
+def test_hdiff_mirror_stores_exact_cells_single_process():
+    """gen_options mirror on the fused PARALLEL tile kernel (hdiff): 8 boxes
+    (the 2-deep faces and corners of the domain) pointed at a scratch field
+    with the identity mapping; after one launch the scratch holds exactly
+    ``out`` on the boxes' cells and is untouched elsewhere, ``out`` is the
+    plain build's (bitwise), and the boxes are consumed by that launch."""
+    import numpy as np
+
+    import oracle
+    import paper_2311_08322_b200 as b200
+    from paper_2311_08322_b200 import native, workloads
+
+    dom = (37, 300, 5)
+    vals = np.random.default_rng(7).uniform(-1, 1, (dom[0] + 4, dom[1] + 4, dom[2]))
+    st_m = b200.compile_stencil(workloads.source("hdiff"), "hdiff", gen_options={"mirror": "out"})
+    inp = b200.from_array(vals, (2, 2, 0))
+    out = b200.allocate("f64", dom, (2, 2, 0), fill="poison")
+    scratch = b200.from_array(np.full((dom[0] + 4, dom[1] + 4, dom[2]), -7.0), (2, 2, 0))
+    ni, nj, _ = dom
+    org = sum(o * s for o, s in zip(scratch.origin, scratch.strides)) * scratch.itemsize
+    boxes = []
+    for di in (-1, 0, 1):
+        for dj in (-1, 0, 1):
+            if di == dj == 0:
+                continue
+            i0, i1 = {-1: (0, 2), 0: (0, ni), 1: (ni - 2, ni)}[di]
+            j0, j1 = {-1: (0, 2), 0: (0, nj), 1: (nj - 2, nj)}[dj]
+            boxes.append((i0, i1, j0, j1, scratch.base_address() + org, *scratch.strides))
+    mod = st_m.build_info["module"]
+    mod.set_mirror(boxes)
+    st_m(inp=inp, coeff=0.05, out=out)
+    native.synchronize(native.default_stream())
+    scratch.mark_device_written()
+    want = oracle.hdiff_c(vals, 0.05)
+    got = out.host_array()[2:-2, 2:-2, :]
+    assert np.array_equal(got, want)
+    s = scratch.host_array()[2:-2, 2:-2, :]
+    band = np.zeros(dom, bool)
+    band[:2], band[-2:], band[:, :2], band[:, -2:] = True, True, True, True
+    assert np.array_equal(s[band], want[band])
+    assert np.all(s[~band] == -7.0)
+    assert np.all(scratch.host_array()[:2] == -7.0) and np.all(scratch.host_array()[:, :2] == -7.0)
+    scratch.view[...] = -9.0
+    scratch.to_device()
+    st_m(inp=inp, coeff=0.05, out=out)
+    scratch.mark_device_written()
+    assert np.all(scratch.host_array() == -9.0)

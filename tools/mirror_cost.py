@@ -1,9 +1,10 @@
 """Cost of the fused halo stores of decomp.PeerFusedStep on one GPU: the
-dycore step (512x512x80 per GPU) with an empty mirror, and with the 8 mirror
-boxes an interior rank of a 3x3 grid has (2-deep faces and corners), here
-pointed at a scratch field on the same GPU instead of the neighbours' halos
-(so the extra pass writes local HBM instead of NVLink).  CUDA-graph timed,
-20 steps per replay, median of 5 replays."""
+dycore step (512x512x80 per GPU; ``--kernel hdiff``: the hdiff ping-pong step
+on the 512x1024x80 C4 tile) with an empty mirror, and with the 8 mirror boxes
+an interior rank of a 3x3 grid has (2-deep faces and corners), here pointed at
+a scratch field on the same GPU instead of the neighbours' halos (so the
+extra stores write local HBM instead of NVLink).  CUDA-graph timed, 20 steps
+per replay, median of 5 replays."""
 import statistics
 import sys
 from pathlib import Path
@@ -12,18 +13,29 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import paper_2311_08322_b200 as b200  # noqa: E402
 from paper_2311_08322_b200 import decomp, native, workloads  # noqa: E402
 
-dom = (512, 512, 80)
+KERNEL = sys.argv[sys.argv.index("--kernel") + 1] if "--kernel" in sys.argv else "dycore"
+dom = (512, 1024, 80) if KERNEL == "hdiff" else (512, 512, 80)
 d = decomp.Decomposition(dom, (1, 1), 0)
-arr = workloads.dycore_arrays(dom, 7)
-opts = {"mirror": "u_out"}
-if len(sys.argv) > 1 and sys.argv[1].isdigit():
-    opts["mirror_batch"] = int(sys.argv[1])
-st = b200.compile_stencil(workloads.source("dycore"), "dycore", gen_options=opts)
-A, B = b200.from_array(arr["u"], (2, 2, 0)), b200.from_array(arr["u"], (2, 2, 0))
-S = b200.from_array(arr["u"], (2, 2, 0))  # scratch "neighbour halo"
-coef = {n: b200.from_array(arr[n]) for n in "abc"}
-step = decomp.PeerFusedStep(st, d, [{"u_in": A, "u_out": B, **coef}, {"u_in": B, "u_out": A, **coef}],
-                            workloads.DYCORE_SCALARS, "u_out", (2, 2))
+if KERNEL == "hdiff":
+    import numpy as np
+
+    u = np.random.default_rng(7).uniform(-1, 1, (dom[0] + 4, dom[1] + 4, dom[2]))
+    opts = {"mirror": "out"}
+    st = b200.compile_stencil(workloads.source("hdiff"), "hdiff", gen_options=opts)
+    A, B, S = (b200.from_array(u, (2, 2, 0)) for _ in range(3))
+    step = decomp.PeerFusedStep(st, d, [{"inp": A, "out": B}, {"inp": B, "out": A}], {"coeff": 0.05},
+                                "out", (2, 2))
+else:
+    arr = workloads.dycore_arrays(dom, 7)
+    opts = {"mirror": "u_out"}
+    if len(sys.argv) > 1 and sys.argv[1].isdigit():
+        opts["mirror_batch"] = int(sys.argv[1])
+    st = b200.compile_stencil(workloads.source("dycore"), "dycore", gen_options=opts)
+    A, B = b200.from_array(arr["u"], (2, 2, 0)), b200.from_array(arr["u"], (2, 2, 0))
+    S = b200.from_array(arr["u"], (2, 2, 0))  # scratch "neighbour halo"
+    coef = {n: b200.from_array(arr[n]) for n in "abc"}
+    step = decomp.PeerFusedStep(st, d, [{"u_in": A, "u_out": B, **coef}, {"u_in": B, "u_out": A, **coef}],
+                                workloads.DYCORE_SCALARS, "u_out", (2, 2))
 ni, nj, _ = dom
 fake = []
 for di in (-1, 0, 1):
@@ -66,4 +78,5 @@ runs = [("no neighbours", []), ("8 neighbours (3x3 interior rank)", fake), ("no 
 if "--split" in sys.argv:
     runs += list(sel.items())
 for label, boxes in runs:
-    print(f"dycore 512x512x80 fused-halo step {opts}, {label}: {timed(boxes):.2f} us/step", flush=True)
+    print(f"{KERNEL} {dom[0]}x{dom[1]}x{dom[2]} fused-halo step {opts}, {label}: {timed(boxes):.2f} us/step",
+          flush=True)

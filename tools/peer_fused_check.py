@@ -1,12 +1,16 @@
 #!/usr/bin/env python
-"""The dycore step (kernels/dycore.gts) decomposed with the halo exchange
-fused into the producing kernel (decomp.PeerFusedStep: the column kernel
-stores its boundary output straight into the neighbours' halos, corners
-included), checked bitwise against the undecomposed oracle, eagerly and
-replayed from a CUDA graph:
+"""A decomposed time loop with the halo exchange fused into the producing
+kernel (decomp.PeerFusedStep: the kernel stores its boundary output straight
+into the neighbours' halos, corners included), checked bitwise against the
+undecomposed oracle, eagerly and replayed from a CUDA graph:
 
     python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 \
-        --master-port P tools/peer_fused_check.py [steps]
+        --master-port P tools/peer_fused_check.py [steps] [--kernel dycore|hdiff]
+
+dycore: kernels/dycore.gts, mirrored by the TMEM column kernel; hdiff: the
+reference's hdiff.gts as a ping-pong loop (out becomes the next step's inp,
+Dirichlet halo), mirrored by the fused PARALLEL tile kernel (BASELINE
+configs[3]'s step with the exchange fused into the producer).
 
 Ranks use GPU LOCAL_RANK % device count (one GPU: they share it through CUDA
 IPC); --timing adds per-step device time (max over ranks).
@@ -34,17 +38,29 @@ def main():
 
     native.set_device(int(os.environ.get("LOCAL_RANK", "0")) % native.device_count())
     grid = decomp.choose_grid(world)
-    gdom = (37 * grid[0] + 3, 70 * grid[1] + 5, 16)
-    arr = workloads.dycore_arrays(gdom, 11)
+    kernel = sys.argv[sys.argv.index("--kernel") + 1] if "--kernel" in sys.argv else "dycore"
+    if kernel == "hdiff":
+        gdom = (37 * grid[0] + 3, 140 * grid[1] + 5, 6)  # several 128-column tiles per rank
+        arr = {"u": np.random.default_rng(11).uniform(-1, 1, (gdom[0] + 4, gdom[1] + 4, gdom[2]))}
+        sc = {"coeff": 0.05}
+        coef = {}
+        fin, fout = "inp", "out"
+        run = lambda n: oracle.hdiff_run(arr["u"], n, 0.05)  # noqa: E731
+    else:
+        gdom = (37 * grid[0] + 3, 70 * grid[1] + 5, 16)
+        arr = workloads.dycore_arrays(gdom, 11)
+        sc = workloads.DYCORE_SCALARS
+        fin, fout = "u_in", "u_out"
+        run = lambda n: oracle.dycore_run(arr["u"], arr["a"], arr["b"], arr["c"], n, **sc)  # noqa: E731
     d = decomp.Decomposition(gdom, grid, rank)
     ni, nj, nk = d.local_domain
     u = d.scatter(arr["u"], (2, 2))
-    coef = {n: b200.from_array(np.array(arr[n][d.i0: d.i1, d.j0: d.j1, :], copy=True)) for n in "abc"}
-    st = b200.compile_stencil(workloads.source("dycore"), "dycore", gen_options={"mirror": "u_out"})
+    if kernel != "hdiff":
+        coef = {n: b200.from_array(np.array(arr[n][d.i0: d.i1, d.j0: d.j1, :], copy=True)) for n in "abc"}
+    st = b200.compile_stencil(workloads.source(kernel), kernel, gen_options={"mirror": fout})
     A, B = b200.from_array(u, (2, 2, 0)), b200.from_array(u, (2, 2, 0))
-    sc = workloads.DYCORE_SCALARS
-    step = decomp.PeerFusedStep(st, d, [{"u_in": A, "u_out": B, **coef}, {"u_in": B, "u_out": A, **coef}],
-                                sc, "u_out", (2, 2))
+    step = decomp.PeerFusedStep(st, d, [{fin: A, fout: B, **coef}, {fin: B, fout: A, **coef}],
+                                sc, fout, (2, 2))
     if os.environ.get("FUSED_NO_MIRROR"):  # negative control: no halo stores -> must fail
         step._boxes = [[] for _ in step._boxes]
     for s in range(steps):
@@ -52,7 +68,7 @@ def main():
     native.synchronize(step.stream)
     last = B if steps % 2 == 1 else A
     got = last.host_array()[2:-2, 2:-2, :]
-    want = oracle.dycore_run(arr["u"], arr["a"], arr["b"], arr["c"], steps, **sc)[2:-2, 2:-2, :]
+    want = run(steps)[2:-2, 2:-2, :]
     ok_e = bool(np.array_equal(got, want[d.i0: d.i1, d.j0: d.j1, :]))
     # graph replay: 2 more steps per replay, 2 replays, against the oracle at steps + 4
     ok_g = True
@@ -63,7 +79,7 @@ def main():
         g.launch()
         native.synchronize(step.stream)
         got = A.host_array()[2:-2, 2:-2, :]
-        want = oracle.dycore_run(arr["u"], arr["a"], arr["b"], arr["c"], steps + 4, **sc)[2:-2, 2:-2, :]
+        want = run(steps + 4)[2:-2, 2:-2, :]
         ok_g = bool(np.array_equal(got, want[d.i0: d.i1, d.j0: d.j1, :]))
     ok = ok_e and ok_g
     extra = ""
@@ -80,7 +96,7 @@ def main():
         extra = f" graph_ms_per_step {e0.elapsed_ms(e1) / 20:.4f}"
     step.close()
     print(("FUSED_PEER_OK " if ok else "FUSED_PEER_FAIL ")
-          + f"rank {rank} grid {grid} local {d.local_domain} steps {steps} bitwise eager {ok_e} graph {ok_g}{extra}",
+          + f"{kernel} rank {rank} grid {grid} local {d.local_domain} steps {steps} bitwise eager {ok_e} graph {ok_g}{extra}",
           flush=True)
     dist.barrier()
     dist.destroy_process_group()
