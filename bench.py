@@ -169,7 +169,7 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons)}
         busy = [s for s in self.samples if s > 0]
         return {"sm_mhz": float(statistics.median(busy or self.samples)), "sm_max_mhz": self.max_mhz,
-                "reasons": sorted(self.reasons - {"gpu_idle"}), "samples": len(self.samples)}
+                "reasons": sorted(self.reasons - {"gpu_idle"})}
 
 
 def host_info():
@@ -809,8 +809,8 @@ def run_b200(args, dist):
         "value": value, "unit": "grid-points/s", "n_gpus": dist.world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": dtype,
-        "data": "synthetic (reference bench generators)",
-        "config": {"workload": SHORT_TEXT[args.workload], "domain_per_gpu": list(domain),
+        "data": "synthetic",
+        "config": {"workload": SHORT_TEXT[args.workload] + (" per GPU" if dist.world > 1 else ""),
                    "parallelism": (f"{dist.world} column shards" if dist.world > 1 else "1 GPU")
                    + (" (shared GPU)" if dist.shared and dist.world > 1 else ""),
                    "l2": f"{r['nsets']} rotating sets > 2x L2",
@@ -822,8 +822,7 @@ def run_b200(args, dist):
                      "alg_bytes": alg, "kernel_us": launch_ms * 1e3},
         "e2e": {"value": dist.world * pts / e2e_val, "unit": "grid-points/s",
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-                "ms": e2e_val * 1e3, "pinned": True,
-                "pageable": {"value": dist.world * pts / pg_val, "ms": pg_val * 1e3}},
+                "ms": e2e_val * 1e3, "pageable": {"value": dist.world * pts / pg_val, "ms": pg_val * 1e3}},
         "clocks": sampler.summary(),
     }
     # Watchdog for the extras (multi-rank exchanges that have not run on this
@@ -856,8 +855,7 @@ def run_b200(args, dist):
             r2 = device_timed(st2, k2, d2, dom2, nst, args.warmup, dist, use_graph=not args.no_graph)
             ach2 = workloads.algorithmic_bytes(k2, dom2, d2) / (r2["launch_ms_mean"] / 1e3) / 1e9
             extra[name] = {"us": r2["launch_ms_mean"] * 1e3, "frac": ach2 / peak,
-                           "parity": parity_check(k2, d2, r2["sets"]),
-                           "launches_per_step": r2["launches_per_step"]}
+                           "parity": parity_check(k2, d2, r2["sets"])}
         # BASELINE configs[0]: hdiff 128x128x64 f64 with the reference gen
         # kernel timed on the same inputs
         dom1 = (128, 128, 64)
@@ -879,7 +877,8 @@ def run_b200(args, dist):
         extra["dycore_fused_peer"] = _extra_guard(dycore_fused_peer, dist)
     if extra and dist.rank == 0:
         detail["extra"] = extra
-        line["extra"] = {k: {kk: vv for kk, vv in v.items() if kk not in ("workload", "unit", "value")}
+        drop = ("workload", "unit", "value", "scaling", "tile", "gpus", "tile_launches_per_step")
+        line["extra"] = {k: {kk: vv for kk, vv in v.items() if kk not in drop}
                          if isinstance(v, dict) else v for k, v in extra.items()}
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
         cores, model = host_info()
@@ -890,7 +889,7 @@ def run_b200(args, dist):
             detail["cpu_rows"] = rows
             line["cpu_baseline"] = {
                 "value": v, "unit": "grid-points/s", "cores": cores, "kind": "reference",
-                "sample": f"median of {len(times)} full-domain calls, reference gen kernel (oracle/_ref)",
+                "sample": f"median of {len(times)} full-domain calls of oracle/_ref",
                 "rows": {k: _r(vv.get("value")) if isinstance(vv, dict) else vv for k, vv in rows.items()},
             }
     done.set()
