@@ -287,6 +287,16 @@ def split_launches(module, domain: tuple, halo: tuple, fields: dict, scalars: di
     return interior, boundary
 
 
+def upload_pending(storages, stream: int) -> None:
+    """Pending host writes land before a capture: an upload (a synchronous
+    copy) cannot be enqueued while the stream is being captured."""
+    seen = set()
+    for st in storages:
+        if id(st) not in seen and hasattr(st, "to_device"):
+            seen.add(id(st))
+            st.to_device(stream)
+
+
 class _GraphReplay:
     """``steps`` steps of a decomposed step replayed from one CUDA graph, or
     (``graph=None``: the capture was refused, e.g. by a NCCL build without
@@ -368,6 +378,7 @@ class DecomposedStep:
         written = [self.fields[name] for name in self.module.written]
         if self.exchanger is not None:
             written.append(self.field)  # its halo is rewritten by the unpack
+        upload_pending(self.fields.values(), self.compute)
         g = self.native.Graph(self.compute)
         try:
             with g.capture():
@@ -565,6 +576,7 @@ class PeerDecomposedStep:
         """``steps`` steps captured once into a CUDA graph on the compute
         stream (the exchange stream joins the capture through the fork / join
         events); replay with ``.launch()``."""
+        upload_pending(self.fields.values(), self.compute)
         g = self.native.Graph(self.compute)
         with g.capture():
             for _ in range(steps):
@@ -751,6 +763,7 @@ class PeerFusedStep:
         starts at the same phase) captured into one CUDA graph."""
         if steps % len(self.phases) or self._step % len(self.phases):
             raise ValueError(f"capture at phase 0, a multiple of {len(self.phases)} steps")
+        upload_pending([st for ph in self.phases for st in ph.values()], self.stream)
         g = self.native.Graph(self.stream)
         start = self._step
         with g.capture():
