@@ -251,6 +251,13 @@ class _Ctx(_MemCtx):
 
 _NOSTORE = False
 _MIRROR = None  # gen_options mirror: api field whose stores also go to neighbour halos
+# gen_options mirror_inline: mirror stores at production (per level, targets
+# resolved per column at tile start) instead of the tile-end pass.  Bitwise
+# (tools/peer_fused_check.py --inline, 2 / 4 processes) but slower
+# (tools/mirror_cost.py, dycore 512^2x80: 185.7 / 193.9 us/step with 0 / 8
+# neighbours against 171-175 / 189 for the pass: the live target registers
+# cost the recurrence), so opt-in.
+_MIRROR_INLINE = False
 
 
 def _emit_stmt(stmt, ctx: _Ctx, ctype, api: set, indent: str, out: list) -> None:
@@ -264,6 +271,14 @@ def _emit_stmt(stmt, ctx: _Ctx, ctype, api: set, indent: str, out: list) -> None
             guard = "valid && v_ == 1234.5678" if _NOSTORE else "valid"  # tmem_debug nostore (timing)
             out.append(f"{indent}  {{ {ctype[name]}* xp_ = colp_{name} + (long long)k * p.f_{name}.sk;"
                        f" if ({guard}) *xp_ = ({ctype[name]})(v_); }}")
+            if _MIRROR_INLINE and name == _MIRROR:
+                # mirror stores at production: this column's resolved targets
+                # (warp-uniform skip for warps without a boundary column)
+                t_ = ctype[name]
+                out.append(f"{indent}  if (wmir_) {{")
+                for m in range(3):
+                    out.append(f"{indent}    if (nmi_ > {m}) mq{m}_[(long long)k * mk{m}_] = ({t_})(v_);")
+                out.append(f"{indent}  }}")
         if name in ctx.cached or name not in api:
             out.append(f"{indent}  cur_{name} = (double)({ctype[name]})(v_);")
         out.append(f"{indent}}}")
@@ -466,9 +481,10 @@ def _emit_variant(kname, plan, sp: ThomasSpec, v: Variant, ctype, dtypes, opts):
     generic per-level-checked body covers partial stages and group
     boundaries."""
     dbg = (opts or {}).get("tmem_debug", "")
-    global _NOSTORE, _MIRROR
+    global _NOSTORE, _MIRROR, _MIRROR_INLINE
     _NOSTORE = dbg == "nostore"
     _MIRROR = (opts or {}).get("mirror") or None
+    _MIRROR_INLINE = bool(_MIRROR) and bool((opts or {}).get("mirror_inline", False))
     impl = plan.impl
     api = {f.name for f in impl.api_fields}
     msf, msb = impl.multistages[sp.ms_f], impl.multistages[sp.ms_b]
@@ -595,6 +611,24 @@ def _emit_variant(kname, plan, sp: ThomasSpec, v: Variant, ctype, dtypes, opts):
     for f in impl.api_fields:
         if any(f.name in writes(st.body) for st in list(msb.stages) + epi_stages):
             w(f"      {ctype[f.name]}* const colp_{f.name} = &GTS_AT(p.f_{f.name}, ic, jc, 0);")
+    if _MIRROR_INLINE:
+        # gen_options mirror_inline: this column's (at most 3) mirror targets,
+        # resolved once per tile; stores follow the column's own (_emit_stmt)
+        t_ = ctype[_MIRROR]
+        w(f"      {t_}* mq0_ = nullptr; {t_}* mq1_ = nullptr; {t_}* mq2_ = nullptr;")
+        w("      long long mk0_ = 0, mk1_ = 0, mk2_ = 0;")
+        w("      int nmi_ = 0;")
+        w("      if (valid) {")
+        w("        for (int d = 0; d < p.mir.n; ++d) {")
+        w("          if (i < p.mir.i0[d] || i >= p.mir.i1[d] || j < p.mir.j0[d] || j >= p.mir.j1[d]) continue;")
+        w(f"          {t_}* const q_ = p.mir.base[d] + (long long)i * p.mir.si[d] + (long long)j * p.mir.sj[d];")
+        w("          if (nmi_ == 0) { mq0_ = q_; mk0_ = p.mir.sk[d]; }")
+        w("          else if (nmi_ == 1) { mq1_ = q_; mk1_ = p.mir.sk[d]; }")
+        w("          else { mq2_ = q_; mk2_ = p.mir.sk[d]; }")
+        w("          ++nmi_;")
+        w("        }")
+        w("      }")
+        w("      const bool wmir_ = __any_sync(0xffffffffu, nmi_ > 0);")
     cf = _caches(msf, 1)
     wf = set()
     for st in msf.stages:
@@ -958,7 +992,7 @@ def _emit_variant(kname, plan, sp: ThomasSpec, v: Variant, ctype, dtypes, opts):
         w("      }")
     if dbg in ("fwdonly", "streamonly"):
         w("      }")
-    if _MIRROR:
+    if _MIRROR and not _MIRROR_INLINE:
         # gen_options mirror: the tile's columns that lie in a neighbour's halo
         # (up to 3: i-face, j-face, corner) send their finished column of the
         # mirrored field there (peer stores), re-read from the tile's own

@@ -28,6 +28,8 @@ if KERNEL == "hdiff":
 else:
     arr = workloads.dycore_arrays(dom, 7)
     opts = {"mirror": "u_out"}
+    if "--inline" in sys.argv:
+        opts["mirror_inline"] = True
     if len(sys.argv) > 1 and sys.argv[1].isdigit():
         opts["mirror_batch"] = int(sys.argv[1])
     st = b200.compile_stencil(workloads.source("dycore"), "dycore", gen_options=opts)

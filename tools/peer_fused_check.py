@@ -57,7 +57,10 @@ def main():
     u = d.scatter(arr["u"], (2, 2))
     if kernel != "hdiff":
         coef = {n: b200.from_array(np.array(arr[n][d.i0: d.i1, d.j0: d.j1, :], copy=True)) for n in "abc"}
-    st = b200.compile_stencil(workloads.source(kernel), kernel, gen_options={"mirror": fout})
+    gopts = {"mirror": fout}
+    if "--inline" in sys.argv:  # the column template's per-level mirror stores (gen_options mirror_inline)
+        gopts["mirror_inline"] = True
+    st = b200.compile_stencil(workloads.source(kernel), kernel, gen_options=gopts)
     A, B = b200.from_array(u, (2, 2, 0)), b200.from_array(u, (2, 2, 0))
     step = decomp.PeerFusedStep(st, d, [{fin: A, fout: B, **coef}, {fin: B, fout: A, **coef}],
                                 sc, fout, (2, 2))
