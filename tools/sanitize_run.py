@@ -7,7 +7,9 @@ Fused PARALLEL tile kernel (hdiff f64 / f32), TMEM column kernels (vadv: W=2
 at nk=20, W=1 at nk=120, generic column kernel at nk=200), the fused dycore
 column kernel and its mirrored-halo build (gen_options mirror), per-stage /
 plane fallbacks (fuse_parallel off), halo pack / unpack and the peer copy-box
-kernel."""
+kernel; round 2: the interior + frame launches of a decomposed step (the thin
+frame variant), the hdiff tile kernel's mirrored halo stores, and the
+read-only L2 eviction kernel."""
 import sys
 from pathlib import Path
 
@@ -79,6 +81,52 @@ band = np.zeros(ddom, bool)
 band[:2], band[-2:], band[:, :2], band[:, -2:] = True, True, True, True
 check("dycore mirrored", np.where(band, scratch.host_array()[2:-2, 2:-2, :], u_out2.host_array()[2:-2, 2:-2, :]),
       oracle.dycore_step(arr["u"], arr["a"], arr["b"], arr["c"], **workloads.DYCORE_SCALARS))
+
+# round 2: interior + frame launches (decomp.split_launches; the frame variant)
+from paper_2311_08322_b200 import decomp  # noqa: E402
+
+for dt, npt in (("f64", np.float64), ("f32", np.float32)):
+    fdom = (37, 300, 3)
+    vals = rng.uniform(-1, 1, (fdom[0] + 4, fdom[1] + 4, fdom[2])).astype(npt)
+    st = b200.compile_stencil(workloads.source("hdiff", dt), "hdiff")
+    inp, out = b200.from_array(vals, (2, 2, 0)), b200.allocate(dt, fdom, fill="poison")
+    inner, frame = decomp.split_launches(st.build_info["module"], fdom, (2, 2), {"inp": inp, "out": out},
+                                         {"coeff": 0.05}, native.default_stream(), True)
+    for go in inner + frame:
+        go()
+    native.synchronize(native.default_stream())
+    check(f"hdiff {dt} interior + frame", out.host_array(), oracle.hdiff_c(vals, 0.05))
+
+# the hdiff tile kernel with mirrored halo stores: 8 boxes into a scratch field
+hdom = (37, 300, 3)
+vals = rng.uniform(-1, 1, (hdom[0] + 4, hdom[1] + 4, hdom[2]))
+shm = b200.compile_stencil(workloads.source("hdiff"), "hdiff", gen_options={"mirror": "out"})
+hin, hout = b200.from_array(vals, (2, 2, 0)), b200.allocate("f64", hdom, (2, 2, 0), fill="poison")
+hscr = b200.from_array(np.zeros((hdom[0] + 4, hdom[1] + 4, hdom[2])), (2, 2, 0))
+horg = sum(o * st_ for o, st_ in zip(hscr.origin, hscr.strides)) * hscr.itemsize
+hboxes = []
+for di in (-1, 0, 1):
+    for dj in (-1, 0, 1):
+        if di or dj:
+            bi = {-1: (0, 2), 0: (0, hdom[0]), 1: (hdom[0] - 2, hdom[0])}[di]
+            bj = {-1: (0, 2), 0: (0, hdom[1]), 1: (hdom[1] - 2, hdom[1])}[dj]
+            hboxes.append((*bi, *bj, hscr.base_address() + horg, *hscr.strides))
+shm.build_info["module"].set_mirror(hboxes)
+shm(inp=hin, coeff=0.05, out=hout)
+native.synchronize(native.default_stream())
+hscr.mark_device_written()
+hband = np.zeros(hdom, bool)
+hband[:2], hband[-2:], hband[:, :2], hband[:, -2:] = True, True, True, True
+hwant = oracle.hdiff_c(vals, 0.05)
+check("hdiff mirrored", np.where(hband, hscr.host_array()[2:-2, 2:-2, :], hout.host_array()[2:-2, 2:-2, :]), hwant)
+
+# the read-only L2 eviction used by tools/ncu_traffic.py
+import ctypes  # noqa: E402
+
+evb = ctypes.c_size_t(0)
+native.call("gts_b200_l2_evict_read", native.default_stream(), ctypes.byref(evb))
+native.synchronize(native.default_stream())
+check("l2 evict read", np.array([evb.value > 0]), np.array([True]))
 
 # halo pack / unpack and the peer copy-box kernel on one device
 f = b200.from_array(rng.uniform(-1, 1, (12, 9, 4)), (2, 2, 0))
