@@ -327,7 +327,7 @@ def run_reference(args, dist):
         "n_gpus": args.gpus, "steps": len(times), "warmup": args.warmup,
         "ms_per_step": total / len(times) * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": dtype, "data": "synthetic",
-        "config": {"workload": CONFIG_TEXT[args.workload], "domain": list(domain), "parallelism": "openmp"},
+        "config": {"workload": SHORT_TEXT[args.workload], "parallelism": f"openmp, {cores} host threads"},
         "cpu_baseline": {"value": value, "unit": "grid-points/s", "cores": cores, "kind": "reference",
                          "sample": f"{len(times)} full-domain calls of the reference gen engine's "
                                    f"generated C kernel (oracle/_ref, -O3 -fopenmp -ffp-contract=off), "
