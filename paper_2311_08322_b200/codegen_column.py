@@ -64,6 +64,7 @@ class ThomasSpec:
     halo: dict = field(default_factory=dict)  # prologue input -> HaloBox
     coop: bool = True  # materialize multi-offset prologue temps cooperatively in smem
     deep_ring: bool = True  # also instantiate the deeper-ring W=2 geometry
+    pro_warps: int = 0  # gen_options pro_warps: prologue warps (0 = consumers evaluate it)
 
 
 @dataclass
@@ -396,7 +397,7 @@ def variants(sp: ThomasSpec, dtypes: dict, geoms_override=None) -> list:
                 rr, cc = rows + hi - li, TJ + hj - lj
                 mat[t] = (half, rr, cc, e, (li, hi, lj, hj))
                 half += -(-(kb * rr * cc * e) // 128) * 128
-        bars = 2 * 8 * nst + 16
+        bars = (3 if sp.pro_warps else 2) * 8 * nst + 16
         free = SMEM_MAX - ring - 2 * half - bars - 64
         sl = max(0, free // (nct * hist_bytes))
         hist_off = ring + 2 * half
@@ -428,6 +429,9 @@ def emit(kname: str, plan, kplan, sp: ThomasSpec, ctype: dict, dtypes: dict, opt
     # measured: the deeper ring helps the fused dycore kernel (181 -> 177 us/step)
     # and costs vadv ~0.9 us at 256^2, so it defaults on with a prologue only
     sp.deep_ring = bool((opts or {}).get("deep_ring", sp.pro is not None))
+    # gen_options pro_warps: the fused prologue runs on its own warps, one
+    # ring stage ahead of the consumers (see _emit_variant)
+    sp.pro_warps = int((opts or {}).get("pro_warps", 0)) if sp.pro is not None and not sp.coop else 0
     for v in variants(sp, dtypes, (opts or {}).get("tmem_geom")):
         if only_w and v.w != int(only_w):
             continue
@@ -491,7 +495,22 @@ def _emit_variant(kname, plan, sp: ThomasSpec, v: Variant, ctype, dtypes, opts):
     rows = 4 * v.w
     ncw = 4 * v.w
     nct = 32 * ncw
-    threads = nct + 32
+    # prologue warps (gen_options pro_warps): warps ncw+1 .. ncw+PW evaluate
+    # the fused prologue for a ring stage as soon as its boxes land and
+    # write the exports over the stage's (then consumed) halo boxes; the
+    # consumers' forward sweep reads them from there (one more mbarrier per
+    # stage).  Needs the exports (binary64 slots) to fit the halo boxes.
+    PW = sp.pro_warps if (sp.pro is not None and v.hbox and not v.mat) else 0
+    slot_off, slot_bytes = {}, v.kb * rows * TJ * 8
+    if PW:
+        h0 = min(v.offs[f] for f in v.hbox)
+        room = sum(v.kb * (rows + hb_.rows_extra) * hb_.cols * hb_.esize for hb_ in v.hbox.values())
+        if rows % PW or len(sp.pro.exports) * slot_bytes > room:
+            PW = 0
+        else:
+            for n_, f in enumerate(sp.pro.exports):
+                slot_off[f] = h0 + n_ * slot_bytes
+    threads = nct + 32 + 32 * PW
     kn = f"{kname}_tmem_w{v.w}" + (f"s{v.nst}" if v.nst != _base_nst(sp, v, dtypes) else "")
     wl = sp.w_level
     hb = 4 * wl
@@ -524,13 +543,20 @@ def _emit_variant(kname, plan, sp: ThomasSpec, v: Variant, ctype, dtypes, opts):
     w(f"  constexpr unsigned STB = {v.stage_bytes}u;")
     w(f"  constexpr int TL = {v.tl};")
     w(f"  unsigned char* hist = smem + {v.hist_off};")
-    w(f"  uint64_t* full = (uint64_t*)(smem + {v.smem_bytes - (2 * 8 * v.nst + 16) - 16});")
+    nbar = 3 if sp.pro_warps else 2  # variants() sized the barrier block
+    w(f"  uint64_t* full = (uint64_t*)(smem + {v.smem_bytes - (nbar * 8 * v.nst + 16) - 16});")
     w("  uint64_t* empty = full + NST;")
-    w("  uint32_t* tslot = (uint32_t*)(empty + NST);")
+    if nbar == 3:
+        w("  uint64_t* pfull = empty + NST;  // prologue exports of a stage written")
+        w("  uint32_t* tslot = (uint32_t*)(pfull + NST);")
+    else:
+        w("  uint32_t* tslot = (uint32_t*)(empty + NST);")
     w("  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;")
     w("  if (warp == 0) gts_tmem_alloc<512>(tslot);")
     w("  if (threadIdx.x == 0) {")
     w(f"    for (int s = 0; s < NST; ++s) {{ gts_mbar_init(&full[s], 1); gts_mbar_init(&empty[s], {ncw}); }}")
+    if PW:
+        w(f"    for (int s = 0; s < NST; ++s) gts_mbar_init(&pfull[s], {PW});")
     w("    gts_fence_mbar_init();")
     w("  }")
     w("  gts_tmem_fence_before_sync();")
@@ -576,6 +602,8 @@ def _emit_variant(kname, plan, sp: ThomasSpec, v: Variant, ctype, dtypes, opts):
     w("        }")
     w("      }")
     w("    }")
+    if PW:
+        _emit_prologue_warps(w, out, sp, v, ctype, ncw, PW, rows, slot_off)
     w("  } else {")
     w(f"    const uint32_t tl = tbase + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)((warp >> 2) * {512 // v.w});")
     w("    const int ct = threadIdx.x;")
@@ -672,7 +700,7 @@ def _emit_variant(kname, plan, sp: ThomasSpec, v: Variant, ctype, dtypes, opts):
     # 4656 instructions), so it is opt-in
     pro_lane = "lane" if (opts or {}).get("pro_shfl", False) else None
 
-    pro_batch = sp.pro is not None and (opts or {}).get("pro_batch", True)
+    pro_batch = sp.pro is not None and (opts or {}).get("pro_batch", True) and not PW
 
     def mat_reads():
         """Phase-B spellings of the materialized temps (this stage's set)."""
@@ -730,7 +758,10 @@ def _emit_variant(kname, plan, sp: ThomasSpec, v: Variant, ctype, dtypes, opts):
         batched: the prologue values were computed by prologue_batch."""
         for f in tracked_f:
             w(f"{indent}double cur_{f} = GTS_NAN;")
-        if batched:
+        if PW and ctx.ring:
+            # written by the prologue warps over this stage's halo boxes
+            ctx.pro_vals = {f: f"pvs_{f}[kk * {rows * TJ}]" for f in sp.pro.exports}
+        elif batched:
             ctx.pro_vals = {f: f"pv_{f}[kk]" for f in sp.pro.exports}
         elif sp.pro is not None:
             # the fused PARALLEL prologue at this thread's (i, j, k)
@@ -772,7 +803,11 @@ def _emit_variant(kname, plan, sp: ThomasSpec, v: Variant, ctype, dtypes, opts):
     w("        const int s = it % NST;")
     w("        const uint32_t ph = (uint32_t)(it / NST) & 1u;")
     w("        gts_mbar_wait(&full[s], ph);")
+    if PW:
+        w("        gts_mbar_wait(&pfull[s], ph);")
     w("        const unsigned char* sb = smem + s * STB;")
+    for f, so in slot_off.items():
+        w(f"        const double* const pvs_{f} = (const double*)(sb + {so}) + warp * {TJ} + lane;")
     for f in sp.streamed:
         w(f"        const {ctype[f]}* const ur_{f} = (const {ctype[f]}*)(sb + {v.offs[f]}) + warp * {TJ} + lane;")
     for f, hbx in v.hbox.items():
@@ -1097,6 +1132,59 @@ def _emit_variant(kname, plan, sp: ThomasSpec, v: Variant, ctype, dtypes, opts):
         return lines
 
     return out, None, call
+
+
+def _emit_prologue_warps(w, out, sp, v, ctype, ncw, PW, rows, slot_off):
+    """Prologue warps: per ring stage, wait for its boxes, evaluate the fused
+    prologue at the tile's rows x 32 columns x KB levels (rows / PW rows per
+    warp, one column per lane), then -- after every prologue warp has read
+    the halo boxes (named barrier 3) -- store the exports over them as
+    binary64 slots [kk][row][lane] and arrive on pfull[s].  The consumers
+    release the stage (empty[s]) only after reading the slots, so the next
+    TMA fill cannot race them; the proxy fence orders these generic stores
+    before that async-proxy overwrite."""
+    rpw = rows // PW
+    kb = v.kb
+    w(f"  }} else if (warp > {ncw}) {{")
+    w(f"    const int pw_ = warp - {ncw + 1};")
+    w("    int it = 0;")
+    w("    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {")
+    w("      for (int kb = 0; kb < nkb; ++kb, ++it) {")
+    w("        const int s = it % NST;")
+    w("        gts_mbar_wait(&full[s], (uint32_t)(it / NST) & 1u);")
+    w("        unsigned char* const sbw = smem + s * STB;")
+    for f in sp.pro.exports:
+        w(f"        double ov_{f}[{kb}][{rpw}];")
+    for rr in range(rpw):
+        w("        {")
+        w(f"          const int prow = pw_ * {rpw} + {rr};")
+        for f, hbx in v.hbox.items():
+            w(f"          const {ctype[f]}* const uh_{f} = (const {ctype[f]}*)(sbw + {v.offs[f]})"
+              f" + (prow - ({hbx.lo_i})) * {hbx.cols} + (lane - ({hbx.bstart}));")
+        w("          #pragma unroll")
+        w(f"          for (int kk = 0; kk < {kb}; ++kk) {{")
+
+        def rd(name, di, dj):
+            hbx = v.hbox[name]
+            off = di * hbx.cols + dj if isinstance(dj, int) else f"{di * hbx.cols} + {dj}"
+            return f"uh_{name}[kk * {(rows + hbx.rows_extra) * hbx.cols} + {off}]"
+        vals = codegen_prologue.emit_point(sp.pro, rd, ctype, out, "            ")
+        for f, var in vals.items():
+            w(f"            ov_{f}[kk][{rr}] = {var};")
+        w("          }")
+        w("        }")
+    w(f'        asm volatile("bar.sync 3, {32 * PW};" ::: "memory");  // halo boxes read by every prologue warp')
+    for f, so in slot_off.items():
+        w(f"        {{ double* const o_ = (double*)(sbw + {so}) + lane;")
+        for rr in range(rpw):
+            for kk in range(kb):
+                w(f"          o_[({kk} * {rows} + pw_ * {rpw} + {rr}) * {TJ}] = ov_{f}[{kk}][{rr}];")
+        w("        }")
+    w("        gts_fence_proxy_async();")
+    w("        __syncwarp();")
+    w("        if (lane == 0) gts_mbar_arrive(&pfull[s]);")
+    w("      }")
+    w("    }")
 
 
 class _EpiCtx(_MemCtx):

@@ -78,6 +78,7 @@ def test_dycore_timeloop_graph_matches_oracle(gpu):
     ({"tmem": False}, 128),           # hdiff launch + generic column kernel
     ({"pro_coop": True}, 128),        # cooperative shared-memory Laplacian (opt-in)
     ({"pro_shfl": True}, 128),        # neighbour-lane shuffles of the Laplacian (opt-in)
+    ({"pro_warps": 4}, 128),          # the prologue on its own warps, exports over the halo boxes
     ({}, 8),                          # TMA-incompatible storages: run-time fallback chain
 ])
 def test_dycore_launch_paths_match_golden(gpu, opts, align):
