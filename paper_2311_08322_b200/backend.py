@@ -26,7 +26,7 @@ from typing import Optional
 
 from . import native
 from ._host import BackendError, Code, ir, sf_common
-from .codegen import entry_name, frame_setter_name, generate_source, mirror_setter_name
+from .codegen import entry_name, frame_setter_name, frame_tile_name, generate_source, mirror_setter_name
 from .lowering import build_plan
 from .storage import DeviceFieldStorage, FieldStorage
 from .toolchain import BuildCache, load_library
@@ -147,6 +147,13 @@ class Module:
             self._frame_fn.restype = ctypes.c_int
         except AttributeError:
             self._frame_fn = None
+        try:
+            ft = getattr(self.lib, frame_tile_name(impl, fp))
+            ft.argtypes, ft.restype = [], ctypes.c_int
+            v_ = int(ft())
+            self.frame_tile = (v_ >> 16, v_ & 0xFFFF)  # rows, columns of a frame tile
+        except AttributeError:
+            self.frame_tile = None
 
     @property
     def frame_supported(self) -> bool:

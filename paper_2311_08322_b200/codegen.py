@@ -472,6 +472,13 @@ def generate_source(plan: Plan, fp, options: Optional[dict] = None) -> str:
         return _generate_source(plan, fp, options)
 
 
+def frame_tile_name(impl, fp) -> str:
+    """Exported query of the frame variant's tile (rows << 16 | columns): the
+    interior launch of a decomposed step covers exactly the frame launch's
+    inner tile rectangle, so no point is computed twice."""
+    return "gts_frametile_" + entry_name(impl, fp)[len("gts_run_"):]
+
+
 def frame_setter_name(impl, fp) -> str:
     """Exported request for a frame launch (decomp.DecomposedStep): the
     calling thread's next launch computes only the tiles that touch the band
@@ -701,6 +708,9 @@ def _generate_source(plan: Plan, fp, options: Optional[dict] = None) -> str:
                 # otherwise the full launch below (idempotent: frame_ok)
                 codeF, preF, launchF = resF
                 out.extend(codeF)
+                out.append('extern "C" __attribute__((visibility("default")))')
+                out.append(f"int {frame_tile_name(impl, fp)}(void) {{ return ({codegen_parallel.TI} << 16) | "
+                           f"{codegen_parallel.TJ}; }}  // frame tile rows, columns")
                 flagF = f"fz_okF_{kidx}"
                 prelude += [ln.replace(f"fz_ok_{kidx}", flagF) for ln in preF]
                 pos = len(launches) - 1

@@ -261,29 +261,59 @@ def call_on_strip(stencil, fields: dict, scalars: dict, offset: tuple, size: tup
     stencil(domain=tuple(size), origin=origins, **fields, **scalars)
 
 
+def frame_interior(domain: tuple, halo: tuple, tile):
+    """Offset and size of the interior launch that complements a frame
+    launch: the frame kernel runs every FTI x FTJ tile outside the inner
+    tile rectangle [ceil(hi/FTI), floor((ni-hi)/FTI)) x [ceil(hj/FTJ),
+    floor((nj-hj)/FTJ)) (codegen_parallel frame variant, ``gts_frame_tile``),
+    so the interior is that rectangle in points; None when it is empty.
+    ``tile`` None (a module without the query): the halo-free interior
+    [hi, ni-hi) x [hj, nj-hj), computed twice where frame tiles overlap it."""
+    ni, nj, nk = domain
+    hi, hj = halo
+    if tile is None:
+        return ((hi, hj), (ni - 2 * hi, nj - 2 * hj, nk)) if ni > 2 * hi and nj > 2 * hj else None
+    ti, tj = tile
+    fi0, fi1 = -(-hi // ti), (ni - hi) // ti
+    fj0, fj1 = -(-hj // tj), (nj - hj) // tj
+    if fi1 <= fi0 or fj1 <= fj0:
+        return None
+    return (fi0 * ti, fj0 * tj), ((fi1 - fi0) * ti, (fj1 - fj0) * tj, nk)
+
+
 def split_launches(module, domain: tuple, halo: tuple, fields: dict, scalars: dict, stream: int,
                    has_neighbours: bool):
     """(interior launchers, boundary launchers) of one decomposed step.
 
-    Without neighbours: one launch of the whole local domain.  Otherwise the
-    interior box [hi, ni-hi) x [hj, nj-hj) (no halo cell read) runs while the
-    halo is in flight, and the rest after it lands:
+    Without neighbours: one launch of the whole local domain.  Otherwise an
+    interior box that reads no halo cell runs while the halo is in flight,
+    and the rest after it lands:
 
     * ONE frame launch when the module supports it (a single fused PARALLEL
       kernel whose recomputation is idempotent, codegen ``frame_ok``): the
       whole domain, enumerating only the thin tiles that touch the band
-      (Module.frame_launcher) -- 2 launches per step;
-    * otherwise the four boundary strips (5 launches per step)."""
+      (Module.frame_launcher), with the interior launch on exactly the
+      frame's inner tile rectangle (``frame_interior``) -- 2 launches per step;
+    * otherwise the interior [hi, ni-hi) x [hj, nj-hj) and the four boundary
+      strips (5 launches per step)."""
     if not has_neighbours:
         return [module.launcher(domain, fields, scalars, stream)], []
     parts = strips(domain, halo)
+    if module.frame_supported and any(name == "interior" for name, _, _ in parts):
+        # the interior launch covers exactly the frame launch's inner tile
+        # rectangle (frame tiles of FTI x FTJ points touching the band are
+        # the frame's): every point is computed once
+        interior = []
+        box = frame_interior(domain, halo, getattr(module, "frame_tile", None))
+        if box is not None:
+            (i0, j0), size = box
+            interior = [module.launcher(size, fields, scalars, stream, (i0, j0, 0))]
+        boundary = [module.frame_launcher(domain, fields, scalars, stream, halo)]
+        return interior, boundary
     interior = [module.launcher(size, fields, scalars, stream, (off[0], off[1], 0))
                 for name, off, size in parts if name in ("interior", "all")]
-    if module.frame_supported and any(name == "interior" for name, _, _ in parts):
-        boundary = [module.frame_launcher(domain, fields, scalars, stream, halo)]
-    else:
-        boundary = [module.launcher(size, fields, scalars, stream, (off[0], off[1], 0))
-                    for name, off, size in parts if name not in ("interior", "all")]
+    boundary = [module.launcher(size, fields, scalars, stream, (off[0], off[1], 0))
+                for name, off, size in parts if name not in ("interior", "all")]
     return interior, boundary
 
 

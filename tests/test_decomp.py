@@ -49,6 +49,33 @@ def test_strips_partition_local_domain():
         assert np.all(cover == 1)
 
 
+@pytest.mark.parametrize("dom", [(512, 1024, 1), (37, 300, 1), (8, 70, 1), (6, 40, 1), (100, 64, 1)])
+@pytest.mark.parametrize("tile", [(4, 32), (2, 32), (8, 128)])
+def test_frame_interior_complements_frame_tiles(dom, tile):
+    """The interior launch (decomp.frame_interior) and the frame launch's
+    tiles (every tile outside the inner rectangle, gts_frame_tile in
+    gts_sm100.cuh) cover the local domain exactly once, and the interior
+    reads no halo cell of a field of extent (2, 2)."""
+    ni, nj, _ = dom
+    hi, hj = 2, 2
+    ti, tj = tile
+    tiles_i, tiles_j = -(-ni // ti), -(-nj // tj)
+    fi0, fi1 = -(-hi // ti), (ni - hi) // ti
+    fj0, fj1 = -(-hj // tj), (nj - hj) // tj
+    fi1, fj1 = max(fi1, fi0), max(fj1, fj0)  # the generated launch's clamp
+    cover = np.zeros(dom[:2], dtype=int)
+    for a in range(tiles_i):
+        for b in range(tiles_j):
+            if not (fi0 <= a < fi1 and fj0 <= b < fj1):
+                cover[a * ti: (a + 1) * ti, b * tj: (b + 1) * tj] += 1
+    box = decomp.frame_interior(dom, (hi, hj), tile)
+    if box is not None:
+        (i0, j0), (si, sj, _) = box
+        assert i0 >= hi and j0 >= hj and i0 + si <= ni - hi and j0 + sj <= nj - hj
+        cover[i0: i0 + si, j0: j0 + sj] += 1
+    assert np.all(cover == 1)
+
+
 def _worker(rank, world, port, q):
     import torch.distributed as dist
 
@@ -450,9 +477,9 @@ def test_fused_step_protocol_model(nranks):
 @pytest.mark.gpu
 @pytest.mark.parametrize("dom", [(512, 1024, 6), (37, 300, 3), (70, 33, 2), (5, 200, 2), (3, 3, 2)])
 def test_interior_plus_frame_launch_bitwise(dom):
-    """decomp.split_launches on one GPU: the interior box launch + ONE frame
-    launch (thin tiles touching the 2-deep band) compute every point exactly
-    like the single full launch (bitwise vs the oracle, output poisoned
+    """decomp.split_launches on one GPU: the interior box launch (the frame's
+    inner tile rectangle) + ONE frame launch (thin tiles touching the 2-deep
+    band) compute every point exactly like the single full launch (bitwise vs the oracle, output poisoned
     first); the frame launch alone writes the whole band."""
     import numpy as np
 
@@ -471,7 +498,9 @@ def test_interior_plus_frame_launch_bitwise(dom):
     fields = {"inp": inp, "out": out}
     interior, boundary = decomp.split_launches(module, dom, (2, 2), fields, {"coeff": 0.05}, stream, True)
     has_interior = dom[0] > 4 and dom[1] > 4
-    assert len(interior) == 1 and len(boundary) == (1 if has_interior else 0)
+    # with a frame launch the interior is its inner tile rectangle (maybe empty)
+    n_int = (1 if decomp.frame_interior(dom, (2, 2), module.frame_tile) else 0) if has_interior else 1
+    assert len(interior) == n_int and len(boundary) == (1 if has_interior else 0)
     n0 = module.launch_count()
     for go in interior + boundary:
         go()
