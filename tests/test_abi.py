@@ -48,6 +48,12 @@ def test_prebuilt_modules_export_entry(kernel, dtype):
     assert hasattr(lib, sym)
     for n in declared("gts_b200_module_"):
         assert hasattr(lib, n), n
+    if kernel == "hdiff":  # a single fused PARALLEL kernel: frame launch + its tile shape
+        short = st.fingerprint.short
+        assert hasattr(lib, f"gts_frame_{kernel}_{short}")
+        ft = getattr(lib, f"gts_frametile_{kernel}_{short}")
+        ft.restype = ctypes.c_int
+        assert (ft() >> 16, ft() & 0xFFFF) == st.build_info["module"].frame_tile == (4, 32)
     # prebuilt by __graft_entry__.build(): served from the in-tree cache
     assert toolchain.COMPILER_INVOCATIONS == before
     assert st.build_info["cache_hit"] is True
