@@ -530,6 +530,12 @@ def _emit_variant(kname, plan, sp: ThomasSpec, v: Variant, ctype, dtypes, opts):
     # round is bandwidth-bound either way) and +1% where no split applies
     # (the runtime level stride), so it is opt-in
     split = not v.hbox and not v.mat and bool((opts or {}).get("col_split", False))
+    # gen_options col_l2pf: L2 prefetch of the next tile's first col_l2pf ring
+    # stages beyond the ring, issued col_l2pf_d stages before this tile's last
+    # stage; col_l2pf0: the first tile's first stages before griddepcontrol.wait
+    l2pf = 0 if split else int((opts or {}).get("col_l2pf", 0))
+    l2pf_d = int((opts or {}).get("col_l2pf_d", 0))
+    l2pf0 = int((opts or {}).get("col_l2pf0", 4 if sp.pro is None else 0))  # measured: vadv 256^2 38.22 -> 36.64 us; dycore neutral
     tm_params = ", ".join(f"const __grid_constant__ CUtensorMap tm_{f}" for f in tm_fields)
     if split:
         tm_params += ", " + ", ".join(f"const __grid_constant__ CUtensorMap tm2_{f}" for f in tm_fields)
@@ -563,6 +569,16 @@ def _emit_variant(kname, plan, sp: ThomasSpec, v: Variant, ctype, dtypes, opts):
     w("  __syncthreads();")
     w("  gts_tmem_fence_after_sync();")
     w("  gts_griddep_launch_dependents();")
+    if l2pf0 and not split:
+        # the first tile's first levels into L2 while the previous grid drains
+        # (an L2 prefetch is coherent with its writes, see gts_tma_prefetch_l2_3d)
+        w(f"  if (warp == {ncw} && lane == 0 && (int)blockIdx.x < ntiles) {{")
+        w(f"    const int jf_ = ((int)blockIdx.x % tiles_j) * {TJ}, if_ = ((int)blockIdx.x / tiles_j) * {rows};")
+        w(f"    for (int q_ = 0; q_ < {l2pf0} && q_ * {KB} < p.nk; ++q_) {{")
+        for f in tm_fields:
+            w(f"      gts_tma_prefetch_l2_3d(&tm_{f}, jf_, if_, q_ * {KB});")
+        w("    }")
+        w("  }")
     w("  gts_griddep_wait();  // PDL: previous grid complete before any global access")
     w("  const uint32_t tbase = *tslot;")
     w("  const int nk = p.nk;")
@@ -599,6 +615,18 @@ def _emit_variant(kname, plan, sp: ThomasSpec, v: Variant, ctype, dtypes, opts):
         w(f"          gts_mbar_arrive_expect_tx(&full[s], {v.tx}u);")
         for f in tm_fields:
             w(f"          gts_tma_load_3d(smem + s * STB + {v.offs[f]}, &tm_{f}, &full[s], j0, i0, kb * {KB});")
+        if l2pf:
+            # warm L2 with the levels of this CTA's next tile that the ring
+            # will not hold when this tile's backward sweep starts, so HBM
+            # keeps streaming while the consumers run it
+            w(f"          if (kb == (nkb - 1 - {l2pf_d} > 0 ? nkb - 1 - {l2pf_d} : 0) && t + (int)gridDim.x < ntiles) {{")
+            w("            const int tn_ = t + (int)gridDim.x;")
+            w(f"            const int jn_ = (tn_ % tiles_j) * {TJ}, in_ = (tn_ / tiles_j) * {rows};")
+            w(f"            for (int q_ = NST; q_ < NST + {l2pf} && q_ < nkb; ++q_) {{")
+            for f in tm_fields:
+                w(f"              gts_tma_prefetch_l2_3d(&tm_{f}, jn_, in_, q_ * {KB});")
+            w("            }")
+            w("          }")
     w("        }")
     w("      }")
     w("    }")

@@ -291,8 +291,9 @@ PDL = "off"  # gen_options pf_pdl: programmatic dependent launch off | early | l
 FRAME = False  # frame variant: the launch enumerates only the tiles outside an inner tile rectangle
 FASTDIV = True  # tile index division by multiply-high (gts_div_c) instead of the XU-pipe division
 MIRROR = None  # gen_options mirror: the buffered api output also stored into neighbour halo boxes
+L2PF0 = 0  # gen_options pf_l2pf0: with PDL, this many of the CTA's first tiles prefetched into L2 before the wait
 DEFAULTS = {"pf_nw": 4, "pf_ri": 8, "pf_vj": 4, "pf_nbuf": 1, "pf_prefetch": 0, "pf_swz": 0, "pf_pdl": "off",
-            "pf_frame": 0, "pf_fastdiv": 1}
+            "pf_frame": 0, "pf_fastdiv": 1, "pf_l2pf0": 0}
 # Measured defaults per element size (profiles/sweep_hdiff_r1.md, hdiff
 # 256x256x80 on one B200, CUDA-graph timed):
 #  f64: 16x128 tiles, double-buffered TMA boxes: 16.9 us vs 18.1 us for
@@ -311,10 +312,15 @@ DEFAULTS = {"pf_nw": 4, "pf_ri": 8, "pf_vj": 4, "pf_nbuf": 1, "pf_prefetch": 0, 
 #  pf_fastdiv (tile index by multiply-high instead of the XU-pipe integer
 #       division; tools/abtest.py, medians of 7): f64 256^2 15.95 -> 15.79 us; f32
 #       15.12 -> 16.28 us (the f32 body schedules worse around it), so off for f32.
+#  pf_l2pf0 (round 2; with PDL, the CTA's first tile prefetched into L2 before
+#       griddepcontrol.wait, so its first TMA load overlaps the previous grid's
+#       tail; tools/abtest.py, medians of 5): f64 256^2 15.70 -> 14.93 us (2 tiles:
+#       16.52), 512x1024 112.6 -> 112.1; f32 with late PDL 15.09 -> 13.72 us
+#       (late PDL alone 15.12, 2 tiles 14.62).
 GEOMETRY = {8: {"pf_nw": 2, "pf_ri": 4, "pf_vj": 4, "pf_nbuf": 2, "pf_prefetch": 1, "pf_swz": 1,
-                "pf_pdl": "late", "pf_fastdiv": 1},
+                "pf_pdl": "late", "pf_fastdiv": 1, "pf_l2pf0": 1},
             4: {"pf_nw": 2, "pf_ri": 8, "pf_vj": 4, "pf_nbuf": 2, "pf_prefetch": 1, "pf_swz": 0,
-                "pf_pdl": "off", "pf_fastdiv": 0}}
+                "pf_pdl": "late", "pf_fastdiv": 0, "pf_l2pf0": 1}}
 
 
 # Large binary64 domains use 4 warps per CTA: in eager launches 512x1024x80 runs
@@ -345,7 +351,7 @@ def configure(opts, esize: int = 0) -> None:
     fingerprint like the reference gen engine's tile options, gen.py:235-238).
     Unset options take the measured default of the group's smallest streamed
     element size ``esize`` (0: the generic DEFAULTS)."""
-    global NW, RI, VJ, TJ, TI, NBUF, PREFETCH, SWZ, PDL, FRAME, FASTDIV
+    global NW, RI, VJ, TJ, TI, NBUF, PREFETCH, SWZ, PDL, FRAME, FASTDIV, L2PF0
     o = dict(DEFAULTS)
     o.update(GEOMETRY.get(esize, {}))
     o.update({k: v for k, v in (opts or {}).items() if k in DEFAULTS})
@@ -355,6 +361,7 @@ def configure(opts, esize: int = 0) -> None:
     PDL = str(o["pf_pdl"])
     FRAME = bool(int(o["pf_frame"]))
     FASTDIV = bool(int(o["pf_fastdiv"]))
+    L2PF0 = int(o["pf_l2pf0"])
     TJ, TI = 32 * VJ, NW * RI
 
 
@@ -404,8 +411,6 @@ def emit(kname: str, plan, kplan, ctype: dict, dtypes: dict, opts=None):
     pdl = PDL  # off | early | late (configure(): per element size, gen_options pf_pdl)
     if pdl == "early":
         w("  gts_griddep_launch_dependents();")
-    if pdl != "off":
-        w("  gts_griddep_wait();  // PDL: previous grid complete before any global access")
     w(f"  const int ni = p.ni, nj = p.nj;")
 
     def tile_coords(tvar, sfx, indent):
@@ -441,6 +446,21 @@ def emit(kname: str, plan, kplan, ctype: dict, dtypes: dict, opts=None):
     # the tensor maps start at the field's extent corner; shifts passed as constants
     for s in streams:
         w(f"  const int jsh_{s.name} = p.tsh_{s.name}_j, ish_{s.name} = p.tsh_{s.name}_i, ksh_{s.name} = p.tsh_{s.name}_k;")
+    if pdl != "off":
+        if L2PF0:
+            # this CTA's first tiles into L2 while the previous grid drains (an
+            # L2 prefetch is coherent with its writes: gts_tma_prefetch_l2_3d)
+            w("  if (threadIdx.x == 0) {")
+            w(f"    for (int m_ = 0; m_ < {L2PF0}; ++m_) {{")
+            w("      const int tp = (int)blockIdx.x + m_ * (int)gridDim.x;")
+            w("      if (tp >= ntiles) break;")
+            tile_coords("tp", "p_", "      ")
+            for s in streams:
+                w(f"      gts_tma_prefetch_l2_3d(&tm_{s.name}, j0p_ + ({s.bstart}) + jsh_{s.name}, "
+                  f"i0p_ + ({geo.min_step + s.rlo}) + ish_{s.name}, kkp_ + ksh_{s.name});")
+            w("    }")
+            w("  }")
+        w("  gts_griddep_wait();  // PDL: previous grid complete before any global access")
     w("  int it = 0;")
     w("  if (threadIdx.x == 0) {")
     for m in range(NBUF - 1):

@@ -87,6 +87,14 @@ __device__ __forceinline__ void gts_tma_load_3d(void* smem_dst, const CUtensorMa
       : "memory");
 }
 
+// Warm L2 with one box (no shared-memory destination, no barrier).  L2 is the
+// point of coherence of device memory, so this is safe even before
+// griddepcontrol.wait: a later write by the previous grid lands in the line.
+__device__ __forceinline__ void gts_tma_prefetch_l2_3d(const CUtensorMap* map, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];"
+               ::"l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2) : "memory");
+}
+
 __device__ __forceinline__ void gts_prefetch_tensormap(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
