@@ -185,3 +185,29 @@ def test_bench_reference_arm_contract():
     assert cb["kind"] == "reference" and cb["cores"] >= 1 and cb["value"] == line["value"] and cb["sample"]
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["d2h_bytes_per_step"] == 0
     assert cb["rows"]["gen_arena_reuse"]["value"] > 0
+
+
+def test_l2_prefetch_before_griddep_wait_in_generated_source():
+    """Round-2 L2 prefetch (K2 "L2 prefetch"): the vadv column
+    kernel and the hdiff tile kernel prefetch their first tile into L2 before
+    griddepcontrol.wait, the column kernel also after the second tile's ring
+    fill; the fused dycore kernel (prologue) and explicit opt-outs do not."""
+
+    def kernel_body(kernel, dtype, name, opts=None):
+        st = b200.compile_stencil(workloads.source(kernel, dtype), kernel, gen_options=opts)
+        src = Path(st.build_info["source_path"]).read_text()
+        m = re.search(r"__global__ void __launch_bounds__\([^)]*\) " + name + r"\(", src)
+        assert m, name
+        end = src.find("\n__global__", m.end())
+        return src[m.end():end if end > 0 else len(src)]
+
+    for kernel, dtype, name in (("vadv", "f64", "gts_k0_column_tmem_w2"), ("hdiff", "f64", "gts_k0_pfused"),
+                                ("hdiff", "f32", "gts_k0_pfused")):
+        body = kernel_body(kernel, dtype, name)
+        pf, wait = body.find("gts_tma_prefetch_l2_3d"), body.find("gts_griddep_wait()")
+        assert 0 <= pf < wait, (kernel, dtype)
+    body = kernel_body("vadv", "f64", "gts_k0_column_tmem_w2")
+    assert "ntiles <= 2 * (int)gridDim.x" in body
+    off = kernel_body("vadv", "f64", "gts_k0_column_tmem_w2", {"col_l2pf0": 0, "col_l2pf": 0})
+    assert "gts_tma_prefetch_l2_3d" not in off
+    assert "gts_tma_prefetch_l2_3d" not in kernel_body("dycore", "f64", "gts_k1_column_tmem_w2s4")

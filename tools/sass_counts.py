@@ -5,7 +5,7 @@
 
 Runs ``cuobjdump -sass`` on the prebuilt benchmark modules (the in-tree
 module cache) and counts, per kernel, the instructions that prove the
-Blackwell paths (TMA loads / stores UTMALDG / UTMASTG, Tensor Memory
+Blackwell paths (TMA loads / L2 prefetches / stores UTMALDG / UTMAPF / UTMASTG, Tensor Memory
 STTM / LDTM, mbarrier SYNCS.*), the FP64 arithmetic (DADD, DMUL, DFMA: the
 parity build has no contraction, so DFMA appears only in the exact-replay
 division of gts_common.cuh), and the XU-pipe conversions (F2F) and MUFU.
@@ -20,7 +20,7 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import paper_2311_08322_b200 as b200  # noqa: E402
 from paper_2311_08322_b200 import workloads  # noqa: E402
 
-OPS = ["UTMALDG", "UTMASTG", "UBLKCP", "STTM", "LDTM", "SYNCS", "DADD", "DMUL", "DFMA", "F2F", "MUFU",
+OPS = ["UTMALDG", "UTMAPF", "UTMASTG", "UBLKCP", "STTM", "LDTM", "SYNCS", "DADD", "DMUL", "DFMA", "F2F", "MUFU",
        "LDS", "STS", "STG", "LDG", "SHFL"]
 MODULES = [("hdiff", "f64", None), ("hdiff", "f32", None), ("vadv", "f64", None), ("vadv", "f32", None),
            ("dycore", "f64", None), ("dycore", "f64", {"mirror": "u_out"})]
