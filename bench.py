@@ -600,6 +600,11 @@ def c4_weak_scaling(dist, args, tile=(512, 1024, 80)):
     ms_s, _, _, lps_s = decomposed_hdiff(dist, nst, args.warmup, tile=tile, transport="none", split=True)
     out["split_us"] = ms_s * 1e3
     out["split_launches_per_step"] = lps_s
+    # the same with the band only on the sides a middle rank of the 4x2 grid
+    # has neighbours on (decomp.neighbour_sides: both i sides, one j side)
+    ms_s2, _, _, _ = decomposed_hdiff(dist, nst, args.warmup, tile=tile, transport="none",
+                                      split=(True, True, True, False))
+    out["split_4x2_us"] = ms_s2 * 1e3
     # (ranks sharing one GPU -- GTS_BENCH_SHARED_GPU -- exercise the peer
     # transports only: NCCL cannot put two ranks on one device)
     transports = (("peer", "fused") if dist.shared else ("nccl", "peer", "fused")) if dist.world > 1 else ()

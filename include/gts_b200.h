@@ -63,15 +63,17 @@ unsigned long long gts_b200_module_launch_count(void);
 
 /* Optional per-module entries (named like the entry: gts_<kind>_<stencil
  * name>_<digest8>), present when the plan allows them:
- *   int gts_frame_<..>(int hi, int hj)      -- the calling thread's next call
- *       runs only the frame tiles touching the (hi, hj) band (single fused
+ *   int gts_frame_<..>(int ilo, int ihi, int jlo, int jhi) -- the calling
+ *       thread's next call runs only the frame tiles touching the band of
+ *       width ilo / ihi / jlo / jhi along the low-i / high-i / low-j / high-j
+ *       side (0: no band on that side, e.g. no neighbour there) (single fused
  *       PARALLEL kernel with idempotent recomputation);
  *   int gts_frametile_<..>(void)            -- the frame tile shape,
  *       rows << 16 | columns (sizes the complementary interior launch);
  *   int gts_mirror_<..>(int n, const int64_t* boxes) -- up to 8 halo-mirror
  *       boxes {i0, i1, j0, j1, base, s_i, s_j, s_k} for the calling thread's
  *       next call (gen_options mirror). */
-typedef int (*gts_b200_frame_fn)(int hi, int hj);
+typedef int (*gts_b200_frame_fn)(int ilo, int ihi, int jlo, int jhi);
 typedef int (*gts_b200_frametile_fn)(void);
 typedef int (*gts_b200_mirror_fn)(int n, const int64_t* boxes);
 

@@ -143,7 +143,7 @@ class Module:
             self._mirror_fn = None
         try:  # present for single fused PARALLEL kernels (codegen frame_ok)
             self._frame_fn = getattr(self.lib, frame_setter_name(impl, fp))
-            self._frame_fn.argtypes = [ctypes.c_int, ctypes.c_int]
+            self._frame_fn.argtypes = [ctypes.c_int] * 4
             self._frame_fn.restype = ctypes.c_int
         except AttributeError:
             self._frame_fn = None
@@ -225,15 +225,18 @@ class Module:
     def frame_launcher(self, domain, fields: dict, scalars: dict, stream: int, band) -> callable:
         """Like ``launcher`` over the whole domain, but every enqueue first
         requests a frame launch for the calling thread: only the tiles with a
-        point inside the band of width ``band`` = (hi, hj) along the domain's
-        sides run (the rest is the interior launch's)."""
+        point inside the band along the domain's sides run (the rest is the
+        interior launch's).  ``band`` = (ilo, ihi, jlo, jhi): the band's width
+        along the low-i, high-i, low-j and high-j sides (0 = none there), or
+        (hi, hj) for the same widths on both sides of each axis."""
         if self._frame_fn is None:
             raise BackendError(Code.COMPILE_FAILED, f"{self.symbol}: no frame launch for this plan")
         go = self.launcher(domain, fields, scalars, stream)
-        fr, hi, hj = self._frame_fn, int(band[0]), int(band[1])
+        bands = frame_bands(band)
+        fr = self._frame_fn
 
         def go_frame() -> None:
-            native.check(fr(hi, hj), "frame request")
+            native.check(fr(*bands), "frame request")
             go()
 
         return go_frame
@@ -253,6 +256,16 @@ class Module:
         status = self.fn(*args)
         if status:
             raise native.DeviceError(status, f"{self.symbol}")
+
+
+def frame_bands(band) -> tuple:
+    """(ilo, ihi, jlo, jhi) band widths from (hi, hj) or a 4-tuple."""
+    b = tuple(int(x) for x in band)
+    if len(b) == 2:
+        b = (b[0], b[0], b[1], b[1])
+    if len(b) != 4 or min(b) < 0:
+        raise ValueError(f"frame band {band!r}: (hi, hj) or (ilo, ihi, jlo, jhi), all >= 0")
+    return b
 
 
 # Per-call state lives in thread-local storage, never in module globals, so

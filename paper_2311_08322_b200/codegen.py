@@ -590,11 +590,13 @@ def _generate_source(plan: Plan, fp, options: Optional[dict] = None) -> str:
     frame_ok = (len(plan.kernels) == 1 and plan.kernels[0].kind == "pfused"
                 and not (api_reads & api_written) and opts.get("pf_frame_variant", True))
     if frame_ok:
-        w("static thread_local int g_frame_hi = -1, g_frame_hj = -1;")
+        # per side: bands of width ilo / ihi / jlo / jhi along the low-i,
+        # high-i, low-j, high-j sides (0: no band, e.g. no neighbour there)
+        w("static thread_local int g_frame_ilo = -1, g_frame_ihi = -1, g_frame_jlo = -1, g_frame_jhi = -1;")
         w('extern "C" __attribute__((visibility("default")))')
-        w(f"int {frame_setter_name(impl, fp)}(int hi, int hj) {{")
-        w("  if (hi < 0 || hj < 0) return %d;" % GTS_ERR_UNSUPPORTED)
-        w("  g_frame_hi = hi; g_frame_hj = hj;  // the calling thread's NEXT launch only")
+        w(f"int {frame_setter_name(impl, fp)}(int ilo, int ihi, int jlo, int jhi) {{")
+        w("  if (ilo < 0 || ihi < 0 || jlo < 0 || jhi < 0) return %d;" % GTS_ERR_UNSUPPORTED)
+        w("  g_frame_ilo = ilo; g_frame_ihi = ihi; g_frame_jlo = jlo; g_frame_jhi = jhi;  // the calling thread's NEXT launch only")
         w("  return 0;")
         w("}")
         w("")
@@ -720,7 +722,7 @@ def _generate_source(plan: Plan, fp, options: Optional[dict] = None) -> str:
                     pos -= 1
                     while not launches[pos].startswith("  if ("):
                         pos -= 1
-                launches[pos:pos] = [f"  if (fr_hi >= 0 && {flagF}) {{"] + launchF + ["  } else"]
+                launches[pos:pos] = [f"  if (fr_ilo >= 0 && {flagF}) {{"] + launchF + ["  } else"]
             if fused_col is not None:
                 pf_lines = launches
                 launches = saved_launches
@@ -831,8 +833,8 @@ def _generate_source(plan: Plan, fp, options: Optional[dict] = None) -> str:
     for s in impl.api_scalars:
         w(f"  p.sc_{s.name} = sc_{s.name};")
     if frame_ok:
-        w("  const int fr_hi = g_frame_hi, fr_hj = g_frame_hj;  // consumed by this launch")
-        w("  g_frame_hi = g_frame_hj = -1;")
+        w("  const int fr_ilo = g_frame_ilo, fr_ihi = g_frame_ihi, fr_jlo = g_frame_jlo, fr_jhi = g_frame_jhi;  // consumed by this launch")
+        w("  g_frame_ilo = g_frame_ihi = g_frame_jlo = g_frame_jhi = -1;")
     if mirror:
         # the boxes apply to this launch only (set again before every launch)
         w("  p.mir = g_mirror;")

@@ -726,12 +726,14 @@ def emit(kname: str, plan, kplan, ctype: dict, dtypes: dict, opts=None):
         ]
     tm_args = ", ".join(f"tm_{kname}_{s.name}" for s in streams)
     if FRAME:
-        # inner tile rectangle: tiles whose points all lie at least (fr_hi, fr_hj)
-        # inside the domain (they need no halo cell of a field of that extent)
+        # inner tile rectangle: tiles whose points all lie at least the band
+        # width of their side inside the domain (they need no halo cell of a
+        # field of that extent); a side without a band reaches the domain edge
+        # (its last partial tile included: decomp.frame_interior clips it)
         tiles = [
             "      const int tiles_i = (int)((ni + %d) / %d), tiles_j = (int)((nj + %d) / %d);" % (TI - 1, TI, TJ - 1, TJ),
-            "      int fi0 = (fr_hi + %d) / %d, fi1 = ((int)ni - fr_hi) / %d;" % (TI - 1, TI, TI),
-            "      int fj0 = (fr_hj + %d) / %d, fj1 = ((int)nj - fr_hj) / %d;" % (TJ - 1, TJ, TJ),
+            "      int fi0 = (fr_ilo + %d) / %d, fi1 = fr_ihi ? ((int)ni - fr_ihi) / %d : tiles_i;" % (TI - 1, TI, TI),
+            "      int fj0 = (fr_jlo + %d) / %d, fj1 = fr_jhi ? ((int)nj - fr_jhi) / %d : tiles_j;" % (TJ - 1, TJ, TJ),
             "      if (fi1 < fi0) fi1 = fi0;",
             "      if (fj1 < fj0) fj1 = fj0;",
             "      const int nkr = k1 - k0;",

@@ -261,33 +261,49 @@ def call_on_strip(stencil, fields: dict, scalars: dict, offset: tuple, size: tup
     stencil(domain=tuple(size), origin=origins, **fields, **scalars)
 
 
-def frame_interior(domain: tuple, halo: tuple, tile):
+def frame_interior(domain: tuple, band, tile):
     """Offset and size of the interior launch that complements a frame
-    launch: the frame kernel runs every FTI x FTJ tile outside the inner
-    tile rectangle [ceil(hi/FTI), floor((ni-hi)/FTI)) x [ceil(hj/FTJ),
-    floor((nj-hj)/FTJ)) (codegen_parallel frame variant, ``gts_frame_tile``),
-    so the interior is that rectangle in points; None when it is empty.
-    ``tile`` None (a module without the query): the halo-free interior
-    [hi, ni-hi) x [hj, nj-hj), computed twice where frame tiles overlap it."""
+    launch.  ``band`` = (hi, hj), or per side (ilo, ihi, jlo, jhi) with 0 for
+    a side that needs none (no neighbour there).  The frame kernel runs every
+    FTI x FTJ tile outside the inner tile rectangle [ceil(ilo/FTI),
+    floor((ni-ihi)/FTI)) x [ceil(jlo/FTJ), floor((nj-jhi)/FTJ)) -- a side
+    without a band reaches the last (partial) tile -- (codegen_parallel frame
+    variant, ``gts_frame_tile``), so the interior is that rectangle in points,
+    clipped to the domain; None when it is empty.  ``tile`` None (a module
+    without the query): the halo-free interior, computed twice where frame
+    tiles overlap it."""
+    from .backend import frame_bands
+
     ni, nj, nk = domain
-    hi, hj = halo
+    ilo, ihi, jlo, jhi = frame_bands(band)
     if tile is None:
-        return ((hi, hj), (ni - 2 * hi, nj - 2 * hj, nk)) if ni > 2 * hi and nj > 2 * hj else None
+        i0, i1, j0, j1 = ilo, ni - ihi, jlo, nj - jhi
+        return ((i0, j0), (i1 - i0, j1 - j0, nk)) if i1 > i0 and j1 > j0 else None
     ti, tj = tile
-    fi0, fi1 = -(-hi // ti), (ni - hi) // ti
-    fj0, fj1 = -(-hj // tj), (nj - hj) // tj
+    fi0, fi1 = -(-ilo // ti), ((ni - ihi) // ti if ihi else -(-ni // ti))
+    fj0, fj1 = -(-jlo // tj), ((nj - jhi) // tj if jhi else -(-nj // tj))
     if fi1 <= fi0 or fj1 <= fj0:
         return None
-    return (fi0 * ti, fj0 * tj), ((fi1 - fi0) * ti, (fj1 - fj0) * tj, nk)
+    i0, j0 = fi0 * ti, fj0 * tj
+    return (i0, j0), (min(fi1 * ti, ni) - i0, min(fj1 * tj, nj) - j0, nk)
+
+
+def neighbour_sides(decomposition) -> tuple:
+    """(low-i, high-i, low-j, high-j): whether a neighbour lies on that side."""
+    return tuple(decomposition.neighbour(di, dj) is not None
+                 for di, dj in ((-1, 0), (1, 0), (0, -1), (0, 1)))
 
 
 def split_launches(module, domain: tuple, halo: tuple, fields: dict, scalars: dict, stream: int,
-                   has_neighbours: bool):
+                   has_neighbours):
     """(interior launchers, boundary launchers) of one decomposed step.
 
-    Without neighbours: one launch of the whole local domain.  Otherwise an
-    interior box that reads no halo cell runs while the halo is in flight,
-    and the rest after it lands:
+    ``has_neighbours``: a bool (all four sides or none) or per side (low-i,
+    high-i, low-j, high-j; ``neighbour_sides``).  Without neighbours: one
+    launch of the whole local domain.  Otherwise an interior box that reads
+    no halo cell of a side with a neighbour runs while the halo is in
+    flight, and the rest after it lands (a side without a neighbour keeps
+    its static boundary halo, so the interior reaches it):
 
     * ONE frame launch when the module supports it (a single fused PARALLEL
       kernel whose recomputation is idempotent, codegen ``frame_ok``): the
@@ -296,19 +312,22 @@ def split_launches(module, domain: tuple, halo: tuple, fields: dict, scalars: di
       frame's inner tile rectangle (``frame_interior``) -- 2 launches per step;
     * otherwise the interior [hi, ni-hi) x [hj, nj-hj) and the four boundary
       strips (5 launches per step)."""
-    if not has_neighbours:
+    sides = (has_neighbours,) * 4 if isinstance(has_neighbours, bool) else tuple(bool(x) for x in has_neighbours)
+    if not any(sides):
         return [module.launcher(domain, fields, scalars, stream)], []
     parts = strips(domain, halo)
     if module.frame_supported and any(name == "interior" for name, _, _ in parts):
         # the interior launch covers exactly the frame launch's inner tile
         # rectangle (frame tiles of FTI x FTJ points touching the band are
         # the frame's): every point is computed once
+        hi, hj = halo
+        band = (hi * sides[0], hi * sides[1], hj * sides[2], hj * sides[3])
         interior = []
-        box = frame_interior(domain, halo, getattr(module, "frame_tile", None))
+        box = frame_interior(domain, band, getattr(module, "frame_tile", None))
         if box is not None:
             (i0, j0), size = box
             interior = [module.launcher(size, fields, scalars, stream, (i0, j0, 0))]
-        boundary = [module.frame_launcher(domain, fields, scalars, stream, halo)]
+        boundary = [module.frame_launcher(domain, fields, scalars, stream, band)]
         return interior, boundary
     interior = [module.launcher(size, fields, scalars, stream, (off[0], off[1], 0))
                 for name, off, size in parts if name in ("interior", "all")]
@@ -355,10 +374,11 @@ class DecomposedStep:
     the NCCL calls included -- into one CUDA graph."""
 
     def __init__(self, stencil, decomposition: Decomposition, fields: dict, scalars: dict,
-                 halo_field: str, halo: tuple, split: Optional[bool] = None):
+                 halo_field: str, halo: tuple, split=None):
         """``split``: interior + frame launches even without neighbours (the
-        1-GPU measurement of what the split costs; default: only with
-        neighbours)."""
+        1-GPU measurement of what the split costs): True for all four sides,
+        or per side (low-i, high-i, low-j, high-j); default: the sides that
+        have a neighbour (``neighbour_sides``)."""
         import torch
 
         from . import native
@@ -379,7 +399,7 @@ class DecomposedStep:
             self.field = fields[halo_field]
             self._comm_t = torch.cuda.ExternalStream(self.comm)
         self.interior, self.boundary = split_launches(self.module, dom, halo, fields, scalars, self.compute,
-                                                      has_nb if split is None else split)
+                                                      neighbour_sides(decomposition) if split is None else split)
         self.launches_per_step = len(self.interior) + len(self.boundary)
         self._ev_start, self._ev_halo = native.Event(), native.Event()
 
@@ -598,7 +618,8 @@ class PeerDecomposedStep:
         self.fields = fields
         self.written = sorted(module.written)
         self.interior, self.boundary = split_launches(module, dom, halo, fields, scalars, self.compute,
-                                                      bool(self.exchanger.peer))
+                                                      neighbour_sides(decomposition) if self.exchanger.peer
+                                                      else False)
         self.launches_per_step = len(self.interior) + len(self.boundary)
         self._ev_start, self._ev_halo = native.Event(), native.Event()
 

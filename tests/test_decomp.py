@@ -51,29 +51,44 @@ def test_strips_partition_local_domain():
 
 @pytest.mark.parametrize("dom", [(512, 1024, 1), (37, 300, 1), (8, 70, 1), (6, 40, 1), (100, 64, 1)])
 @pytest.mark.parametrize("tile", [(4, 32), (2, 32), (8, 128)])
-def test_frame_interior_complements_frame_tiles(dom, tile):
+@pytest.mark.parametrize("sides", [(1, 1, 1, 1), (0, 1, 1, 0), (1, 0, 0, 1), (0, 0, 0, 1), (1, 1, 0, 0)])
+def test_frame_interior_complements_frame_tiles(dom, tile, sides):
     """The interior launch (decomp.frame_interior) and the frame launch's
     tiles (every tile outside the inner rectangle, gts_frame_tile in
-    gts_sm100.cuh) cover the local domain exactly once, and the interior
-    reads no halo cell of a field of extent (2, 2)."""
+    gts_sm100.cuh; the rectangle as the generated launch computes it) cover
+    the local domain exactly once, and the interior reads no halo cell of a
+    field of extent (2, 2) on a side with a band (a neighbour); sides without
+    one let the interior reach the domain edge."""
     ni, nj, _ = dom
-    hi, hj = 2, 2
+    ilo, ihi, jlo, jhi = (2 * sides[0], 2 * sides[1], 2 * sides[2], 2 * sides[3])
     ti, tj = tile
     tiles_i, tiles_j = -(-ni // ti), -(-nj // tj)
-    fi0, fi1 = -(-hi // ti), (ni - hi) // ti
-    fj0, fj1 = -(-hj // tj), (nj - hj) // tj
+    fi0, fi1 = -(-ilo // ti), ((ni - ihi) // ti if ihi else tiles_i)
+    fj0, fj1 = -(-jlo // tj), ((nj - jhi) // tj if jhi else tiles_j)
     fi1, fj1 = max(fi1, fi0), max(fj1, fj0)  # the generated launch's clamp
     cover = np.zeros(dom[:2], dtype=int)
     for a in range(tiles_i):
         for b in range(tiles_j):
             if not (fi0 <= a < fi1 and fj0 <= b < fj1):
                 cover[a * ti: (a + 1) * ti, b * tj: (b + 1) * tj] += 1
-    box = decomp.frame_interior(dom, (hi, hj), tile)
+    box = decomp.frame_interior(dom, (ilo, ihi, jlo, jhi), tile)
     if box is not None:
         (i0, j0), (si, sj, _) = box
-        assert i0 >= hi and j0 >= hj and i0 + si <= ni - hi and j0 + sj <= nj - hj
+        assert i0 >= ilo and j0 >= jlo and i0 + si <= ni - ihi and j0 + sj <= nj - jhi
         cover[i0: i0 + si, j0: j0 + sj] += 1
     assert np.all(cover == 1)
+    if sides == (1, 1, 1, 1):  # the (hi, hj) spelling is the same band
+        assert decomp.frame_interior(dom, (2, 2), tile) == box
+
+
+def test_neighbour_sides():
+    """decomp.neighbour_sides on a 4x2 grid: corner, edge and interior ranks."""
+    g = (2048, 2048, 80)
+    sides = {r: decomp.neighbour_sides(decomp.Decomposition(g, (4, 2), r)) for r in range(8)}
+    assert sides[0] == (False, True, False, True)
+    assert sides[3] == (True, True, True, False)
+    assert sides[7] == (True, False, True, False)
+    assert decomp.neighbour_sides(decomp.Decomposition(g, (1, 1), 0)) == (False,) * 4
 
 
 def _worker(rank, world, port, q):
@@ -476,11 +491,14 @@ def test_fused_step_protocol_model(nranks):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("dom", [(512, 1024, 6), (37, 300, 3), (70, 33, 2), (5, 200, 2), (3, 3, 2)])
-def test_interior_plus_frame_launch_bitwise(dom):
+@pytest.mark.parametrize("sides", [True, (False, True, True, False), (True, False, False, False)])
+def test_interior_plus_frame_launch_bitwise(dom, sides):
     """decomp.split_launches on one GPU: the interior box launch (the frame's
     inner tile rectangle) + ONE frame launch (thin tiles touching the 2-deep
-    band) compute every point exactly like the single full launch (bitwise vs the oracle, output poisoned
-    first); the frame launch alone writes the whole band."""
+    band on the sides with a neighbour: all four, or per side as
+    decomp.neighbour_sides gives them) compute every point exactly like the
+    single full launch (bitwise vs the oracle, output poisoned first); the
+    frame launch alone writes the whole band."""
     import numpy as np
 
     import oracle
@@ -496,10 +514,12 @@ def test_interior_plus_frame_launch_bitwise(dom):
     stream = native.default_stream()
     out = b200.allocate("f64", dom, fill="poison")
     fields = {"inp": inp, "out": out}
-    interior, boundary = decomp.split_launches(module, dom, (2, 2), fields, {"coeff": 0.05}, stream, True)
+    interior, boundary = decomp.split_launches(module, dom, (2, 2), fields, {"coeff": 0.05}, stream, sides)
     has_interior = dom[0] > 4 and dom[1] > 4
+    sd = (True,) * 4 if sides is True else sides
+    bands = tuple(2 * int(x) for x in sd)
     # with a frame launch the interior is its inner tile rectangle (maybe empty)
-    n_int = (1 if decomp.frame_interior(dom, (2, 2), module.frame_tile) else 0) if has_interior else 1
+    n_int = (1 if decomp.frame_interior(dom, bands, module.frame_tile) else 0) if has_interior else 1
     assert len(interior) == n_int and len(boundary) == (1 if has_interior else 0)
     n0 = module.launch_count()
     for go in interior + boundary:
@@ -510,12 +530,13 @@ def test_interior_plus_frame_launch_bitwise(dom):
     if has_interior:
         out2 = b200.allocate("f64", dom, fill="poison")
         fields2 = {"inp": inp, "out": out2}
-        _, frame = decomp.split_launches(module, dom, (2, 2), fields2, {"coeff": 0.05}, stream, True)
+        _, frame = decomp.split_launches(module, dom, (2, 2), fields2, {"coeff": 0.05}, stream, sides)
         frame[0]()
         native.synchronize(stream)
         got = out2.host_array()
-        band = np.ones(dom, bool)
-        band[2:-2, 2:-2, :] = False
+        band = np.zeros(dom, bool)
+        band[:bands[0]], band[dom[0] - bands[1]:] = True, True
+        band[:, :bands[2]], band[:, dom[1] - bands[3]:] = True, True
         assert np.array_equal(got[band], want[band])
         # interior points are either untouched (poison) or the same values
         inner = got[~band]
