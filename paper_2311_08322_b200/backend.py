@@ -37,7 +37,7 @@ BACKEND_ID = "b200"
 # host buffers page-locked in place by the mirror mode: id(numpy base) ->
 # registration (unregistered when the buffer is garbage collected)
 _pinned_in_place: dict = {}
-_pin_lock = threading.Lock()
+_pin_lock = threading.RLock()  # the GC finalizer may run while it is held
 # the reference's own storages are pageable numpy memory (stencilforge
 # storage.py:130-160); pinning them in place on first use turns their copies
 # from the driver's staged pageable path into full-speed DMA
@@ -51,17 +51,22 @@ def _pin_host_buffer(base) -> None:
             return
         reg = ctypes.c_int(0)
         st = native.lib().gts_b200_host_register(base.ctypes.data, base.nbytes, ctypes.byref(reg))
-        _pinned_in_place[key] = bool(reg.value) if st == 0 else False
-        if st == 0 and reg.value:
-            weakref.finalize(base, _unpin_host_buffer, key, base.ctypes.data)
+        registered = st == 0 and bool(reg.value)
+        _pinned_in_place[key] = registered
+        # every entry (also "already page-locked" and "registration failed")
+        # leaves with its buffer: a later buffer that reuses the id must be
+        # looked at again, not taken for one that needs no pinning
+        weakref.finalize(base, _unpin_host_buffer, key, base.ctypes.data, registered)
 
 
-def _unpin_host_buffer(key, ptr) -> None:  # pragma: no cover - GC path
-    _pinned_in_place.pop(key, None)
-    try:
-        native.lib().gts_b200_host_unregister(ptr)
-    except Exception:
-        pass
+def _unpin_host_buffer(key, ptr, registered: bool = True) -> None:  # pragma: no cover - GC path
+    with _pin_lock:
+        _pinned_in_place.pop(key, None)
+    if registered:
+        try:
+            native.lib().gts_b200_host_unregister(ptr)
+        except Exception:
+            pass
 
 
 class _Mirror:

@@ -352,6 +352,7 @@ class Variant:
     mat: dict = field(default_factory=dict)  # materialized prologue temp -> (smem offset in a set, rows, cols, esize, region)
     mat_off: int = 0  # smem offset of the two materialization buffer sets
     mat_half: int = 0  # bytes of one set
+    cps: int = 1  # CTAs per SM (TMEM and shared memory split between them)
 
 
 def variants(sp: ThomasSpec, dtypes: dict, geoms_override=None) -> list:
@@ -365,10 +366,19 @@ def variants(sp: ThomasSpec, dtypes: dict, geoms_override=None) -> list:
     seen = set()
     geoms = ((2, 4, 160 * 1024), (2, 4, 128 * 1024), (1, 8, RING_BUDGET))
     if not sp.deep_ring:
-        geoms = geoms[1:]
-    if geoms_override:  # gen_options tmem_geom: [[w, kb, ring KiB], ...] (experiments)
-        geoms = tuple((int(w), int(kb), int(kib) * 1024) for w, kb, kib in geoms_override)
-    for w, kb, budget in geoms:
+        # without a prologue, two CTAs per SM (W=1, 4-level stages, 64 KiB
+        # rings, TMEM and shared memory halved) first: the two pipelines run
+        # out of phase.  tools/abtest.py (medians of 5 / 3): vadv 256^2 35.58 ->
+        # 35.24 us, 512^2 131.1 -> 129.3, f32 256^2 35.56 -> 35.03; 2- or 8-level
+        # stages and an 80 KiB ring were slower; the dycore kernel (prologue)
+        # measured 175.5 -> 177.9 us/step, so it keeps one CTA per SM
+        geoms = ((1, 4, 64 * 1024, 2),) + geoms[1:]
+    if geoms_override:  # gen_options tmem_geom: [[w, kb, ring KiB(, CTAs per SM)], ...] (experiments)
+        geoms = tuple((int(g[0]), int(g[1]), int(g[2]) * 1024) + tuple(int(x) for x in g[3:4])
+                      for g in geoms_override)
+    for geom in geoms:
+        w, kb, budget = geom[:3]
+        cps = geom[3] if len(geom) > 3 else 1
         rows = 4 * w
         offs, sb = {}, 0
         for f in sp.streamed:
@@ -398,15 +408,15 @@ def variants(sp: ThomasSpec, dtypes: dict, geoms_override=None) -> list:
                 mat[t] = (half, rr, cc, e, (li, hi, lj, hj))
                 half += -(-(kb * rr * cc * e) // 128) * 128
         bars = (3 if sp.pro_warps else 2) * 8 * nst + 16
-        free = SMEM_MAX - ring - 2 * half - bars - 64
+        free = (SMEM_MAX if cps == 1 else SMEM_MAX // cps - 1024) - ring - 2 * half - bars - 64
         sl = max(0, free // (nct * hist_bytes))
         hist_off = ring + 2 * half
         smem = ring + 2 * half + sl * nct * hist_bytes + bars + 16
-        tl = (512 // w) // sp.w_level
-        if nst * sb > budget or (w, nst) in seen:
+        tl = (512 // cps // w) // sp.w_level
+        if nst * sb > budget or (w, nst, cps) in seen or free < 0:
             continue
-        seen.add((w, nst))
-        out.append(Variant(w, kb, nst, sb, offs, tl, sl, smem, hist_off, hboxes, tx, mat, ring, half))
+        seen.add((w, nst, cps))
+        out.append(Variant(w, kb, nst, sb, offs, tl, sl, smem, hist_off, hboxes, tx, mat, ring, half, cps))
     return out
 
 
@@ -511,7 +521,7 @@ def _emit_variant(kname, plan, sp: ThomasSpec, v: Variant, ctype, dtypes, opts):
             for n_, f in enumerate(sp.pro.exports):
                 slot_off[f] = h0 + n_ * slot_bytes
     threads = nct + 32 + 32 * PW
-    kn = f"{kname}_tmem_w{v.w}" + (f"s{v.nst}" if v.nst != _base_nst(sp, v, dtypes) else "")
+    kn = f"{kname}_tmem_w{v.w}" + (f"s{v.nst}" if v.nst != _base_nst(sp, v, dtypes) else "") + (f"c{v.cps}" if v.cps > 1 else "")
     wl = sp.w_level
     hb = 4 * wl
     hoff, o = {}, 0
@@ -546,7 +556,7 @@ def _emit_variant(kname, plan, sp: ThomasSpec, v: Variant, ctype, dtypes, opts):
     w(f"// TMEM column kernel, W={v.w}: {nct} columns/CTA, streamed {sp.streamed} (ring {v.nst} x"
       f" {v.stage_bytes} B), history {sp.cross}: TMEM levels [0,{v.tl}), smem levels"
       f" [{v.tl},{v.tl + v.sl})")
-    w(f"__global__ void __launch_bounds__({threads}, 1) {kn}(const __grid_constant__ GtsParams p, "
+    w(f"__global__ void __launch_bounds__({threads}, {v.cps}) {kn}(const __grid_constant__ GtsParams p, "
       f"{tm_params}, int tiles_j, int ntiles" + (", int n1, int isplit, int h2" if split else "") + ") {")
     w("  extern __shared__ __align__(1024) unsigned char smem[];")
     w(f"  constexpr int NST = {v.nst};")
@@ -562,7 +572,7 @@ def _emit_variant(kname, plan, sp: ThomasSpec, v: Variant, ctype, dtypes, opts):
     else:
         w("  uint32_t* tslot = (uint32_t*)(empty + NST);")
     w("  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;")
-    w("  if (warp == 0) gts_tmem_alloc<512>(tslot);")
+    w(f"  if (warp == 0) gts_tmem_alloc<{512 // v.cps}>(tslot);")
     w("  if (threadIdx.x == 0) {")
     w(f"    for (int s = 0; s < NST; ++s) {{ gts_mbar_init(&full[s], 1); gts_mbar_init(&empty[s], {ncw}); }}")
     if PW:
@@ -650,7 +660,7 @@ def _emit_variant(kname, plan, sp: ThomasSpec, v: Variant, ctype, dtypes, opts):
     if PW:
         _emit_prologue_warps(w, out, sp, v, ctype, ncw, PW, rows, slot_off)
     w("  } else {")
-    w(f"    const uint32_t tl = tbase + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)((warp >> 2) * {512 // v.w});")
+    w(f"    const uint32_t tl = tbase + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)((warp >> 2) * {512 // v.cps // v.w});")
     w("    const int ct = threadIdx.x;")
     w("    int it = 0;")
     gf = _interval_groups(msf)
@@ -1141,7 +1151,7 @@ def _emit_variant(kname, plan, sp: ThomasSpec, v: Variant, ctype, dtypes, opts):
     w("  }")
     w("  gts_tmem_fence_before_sync();")
     w("  __syncthreads();")
-    w("  if (warp == 0) { gts_tmem_fence_after_sync(); gts_tmem_dealloc<512>(tbase); }")
+    w(f"  if (warp == 0) {{ gts_tmem_fence_after_sync(); gts_tmem_dealloc<{512 // v.cps}>(tbase); }}")
     w("}")
 
     def call(vi):
@@ -1150,7 +1160,7 @@ def _emit_variant(kname, plan, sp: ThomasSpec, v: Variant, ctype, dtypes, opts):
             return [
                 f"const int tiles_j = (int)((nj + {TJ - 1}) / {TJ});",
                 f"const int ntiles = tiles_j * (int)((ni + {rows - 1}) / {rows});",
-                "int grid = gts_sm_count(); if (grid > ntiles) grid = ntiles;",
+                f"int grid = {v.cps} * gts_sm_count(); if (grid > ntiles) grid = ntiles;",
                 f"static bool attr_{kn} = false;",
                 f"if (!attr_{kn}) {{ cudaFuncSetAttribute({kn}, cudaFuncAttributeMaxDynamicSharedMemorySize, {v.smem_bytes}); attr_{kn} = true; }}",
                 f"gts_launch_pdl({kn}, dim3(grid), dim3({threads}), {v.smem_bytes}, st, p, {tm_args}, tiles_j, ntiles);",

@@ -201,7 +201,8 @@ def test_l2_prefetch_before_griddep_wait_in_generated_source():
         end = src.find("\n__global__", m.end())
         return src[m.end():end if end > 0 else len(src)]
 
-    for kernel, dtype, name in (("vadv", "f64", "gts_k0_column_tmem_w2"), ("hdiff", "f64", "gts_k0_pfused"),
+    for kernel, dtype, name in (("vadv", "f64", "gts_k0_column_tmem_w1s4c2"), ("vadv", "f64", "gts_k0_column_tmem_w2"),
+                                ("hdiff", "f64", "gts_k0_pfused"),
                                 ("hdiff", "f32", "gts_k0_pfused")):
         body = kernel_body(kernel, dtype, name)
         pf, wait = body.find("gts_tma_prefetch_l2_3d"), body.find("gts_griddep_wait()")
@@ -211,3 +212,36 @@ def test_l2_prefetch_before_griddep_wait_in_generated_source():
     off = kernel_body("vadv", "f64", "gts_k0_column_tmem_w2", {"col_l2pf0": 0, "col_l2pf": 0})
     assert "gts_tma_prefetch_l2_3d" not in off
     assert "gts_tma_prefetch_l2_3d" not in kernel_body("dycore", "f64", "gts_k1_column_tmem_w2s4")
+
+
+def test_pin_in_place_bookkeeping_leaves_with_the_buffer(monkeypatch):
+    """backend._pin_host_buffer: a buffer that needs no pinning (already
+    page-locked) or could not be pinned must not leave a stale entry behind
+    once it is freed -- a later pageable buffer that reuses its id() would
+    otherwise never be page-locked (its copies fall back to the driver's
+    staged path: 3.6 -> 5.7 ms per vadv call measured)."""
+    import gc
+
+    import numpy as np
+
+    from paper_2311_08322_b200 import backend
+
+    calls = []
+
+    class _Lib:
+        def gts_b200_host_register(self, ptr, nbytes, reg):
+            calls.append(ptr)
+            return 0  # "already page-locked": success, nothing registered
+
+        def gts_b200_host_unregister(self, ptr):  # pragma: no cover - must not be called
+            raise AssertionError("unregistered a buffer it did not register")
+
+    monkeypatch.setattr(backend.native, "lib", lambda: _Lib())
+    a = np.zeros(1024)
+    key = id(a)
+    backend._pin_host_buffer(a)
+    backend._pin_host_buffer(a)  # cached while alive
+    assert key in backend._pinned_in_place and backend._pinned_in_place[key] is False and len(calls) == 1
+    del a
+    gc.collect()
+    assert key not in backend._pinned_in_place
