@@ -758,6 +758,47 @@ def dycore_timed(dist, steps=100, domain=(512, 512, 80), reps=3, gen_options=Non
     }
 
 
+# binary32 <-> binary64 conversions (F2F) per SM per clock on this B200: the
+# XU pipe, measured with tools/ubench.cu ("Instruction costs")
+XU_CONV_PER_CLK_SM = 16
+
+
+def conversion_roofline(st, domain, seconds, sampler):
+    """The binding roofline of a binary32 tile kernel (the reference computes
+    f32 programs in binary64, narrowing every store): conversions per point
+    = the F2F count of the fully unrolled thread-tile body of the fused tile
+    kernel (cuobjdump of the loaded module) / the points of one thread-tile,
+    against XU_CONV_PER_CLK_SM x SMs x the SM clock under load.  None when
+    cuobjdump or the kernel is not found."""
+    import re
+    import shutil
+
+    from paper_2311_08322_b200 import codegen_parallel, native
+
+    exe = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    so = st.build_info.get("so_path")
+    if not so or not Path(exe).exists():
+        return None
+    try:
+        sass = subprocess.run([exe, "-sass", so], capture_output=True, text=True, timeout=120).stdout
+    except (OSError, subprocess.SubprocessError):
+        return None
+    body = None
+    for chunk in re.split(r"\n\s+Function : ", sass)[1:]:
+        if chunk.split("\n", 1)[0].strip().startswith("_Z13gts_k0_pfused"):
+            body = chunk
+    if body is None:
+        return None
+    geo = codegen_parallel.GEOMETRY[4]
+    conv = len(re.findall(r"\bF2F\.", body)) / (geo["pf_ri"] * geo["pf_vj"])
+    mhz = sampler.summary().get("sm_mhz") or sampler.summary().get("sm_max_mhz")
+    info = native.device_info()
+    peak = XU_CONV_PER_CLK_SM * info["sm_count"] * mhz * 1e6
+    achieved = conv * domain[0] * domain[1] * domain[2] / seconds
+    return {"bound": "xu (f32<->f64 conversions)", "conv_per_point": round(conv, 3),
+            "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "Tconv/s", "frac": achieved / peak}
+
+
 def _r(x, n=4):
     """Round for the compact JSON line."""
     if isinstance(x, float):
@@ -861,6 +902,10 @@ def run_b200(args, dist):
             ach2 = workloads.algorithmic_bytes(k2, dom2, d2) / (r2["launch_ms_mean"] / 1e3) / 1e9
             extra[name] = {"us": r2["launch_ms_mean"] * 1e3, "frac": ach2 / peak,
                            "parity": parity_check(k2, d2, r2["sets"])}
+            if d2 == "f32":
+                xu = conversion_roofline(st2, dom2, r2["launch_ms_mean"] / 1e3, sampler)
+                if xu:
+                    extra[name]["xu"] = xu
         # BASELINE configs[0]: hdiff 128x128x64 f64 with the reference gen
         # kernel timed on the same inputs
         dom1 = (128, 128, 64)
