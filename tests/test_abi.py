@@ -245,3 +245,29 @@ def test_pin_in_place_bookkeeping_leaves_with_the_buffer(monkeypatch):
     del a
     gc.collect()
     assert key not in backend._pinned_in_place
+
+
+def test_bench_conversion_roofline_from_sass(monkeypatch):
+    """bench.conversion_roofline: the f32 hdiff tile kernel's binary32 <->
+    binary64 conversions per point come from the module's SASS (the fully
+    unrolled thread-tile body), 7.75 with the default geometry,
+    and the fraction is taken against 16 conversions /clk/SM."""
+    import shutil
+    import sys
+
+    if not (shutil.which("cuobjdump") or Path("/usr/local/cuda/bin/cuobjdump").exists()):
+        pytest.skip("cuobjdump unavailable")
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+    import bench
+
+    monkeypatch.setattr(native, "device_info", lambda dev=None: {"sm_count": 148})
+
+    class _S:
+        def summary(self):
+            return {"sm_mhz": 1965.0}
+
+    st = b200.compile_stencil(workloads.source("hdiff", "f32"), "hdiff")
+    r = bench.conversion_roofline(st, (256, 256, 80), 13.7e-6, _S())
+    assert r["conv_per_point"] == 7.75
+    assert abs(r["peak"] - 16 * 148 * 1965e6 / 1e12) < 1e-9
+    assert 0.6 < r["frac"] < 0.7
