@@ -3,8 +3,9 @@
 
     compute-sanitizer --tool memcheck python tools/sanitize_run.py
 
-Fused PARALLEL tile kernel (hdiff f64 / f32), TMEM column kernels (vadv: W=2
-at nk=20, W=1 at nk=120, generic column kernel at nk=200), the fused dycore
+Fused PARALLEL tile kernel (hdiff f64 / f32), TMEM column kernels (vadv: the
+two-CTA W=1 default at nk=20 and over two tile rounds, the W=2 geometry, W=1
+at nk=120, generic column kernel at nk=200), the fused dycore
 column kernel and its mirrored-halo build (gen_options mirror), per-stage /
 plane fallbacks (fuse_parallel off), halo pack / unpack and the peer copy-box
 kernel; round 2: the interior + frame launches of a decomposed step (the thin
@@ -43,13 +44,17 @@ for dt, npt in (("f64", np.float64), ("f32", np.float32)):
         st(inp=inp, coeff=0.05, out=out)
         check(f"hdiff {dt} {opts}", out.host_array(), oracle.hdiff_c(vals, 0.05))
 
-for shape in ((19, 40, 20), (9, 33, 120), (5, 6, 200)):
+# default geometry (two CTAs per SM, W=1) at nk=20, and with two tile rounds
+# (the in-kernel L2 prefetch of the second tile), W=1 at nk=120, the generic
+# column kernel at nk=200, and the one-CTA W=2 geometry explicitly
+for shape, opts in (((19, 40, 20), None), ((160, 256, 8), None), ((9, 33, 120), None), ((5, 6, 200), None),
+                    ((19, 40, 20), {"tmem_geom": [[2, 4, 128]]})):
     a, b, c, d = oracle.make_diagonally_dominant(rng, shape)
-    sv = b200.compile_stencil(workloads.source("vadv"), "vadv")
+    sv = b200.compile_stencil(workloads.source("vadv"), "vadv", gen_options=opts)
     fa = {n: b200.from_array(v) for n, v in zip("abcd", (a, b, c, d))}
     x = b200.allocate("f64", shape)
     sv(x=x, **fa)
-    check(f"vadv {shape}", x.host_array(), oracle.vadv_c(a, b, c, d))
+    check(f"vadv {shape} {opts}", x.host_array(), oracle.vadv_c(a, b, c, d))
 
 ddom = (20, 40, 12)
 arr = workloads.dycore_arrays(ddom, 3)
@@ -90,12 +95,14 @@ for dt, npt in (("f64", np.float64), ("f32", np.float32)):
     vals = rng.uniform(-1, 1, (fdom[0] + 4, fdom[1] + 4, fdom[2])).astype(npt)
     st = b200.compile_stencil(workloads.source("hdiff", dt), "hdiff")
     inp, out = b200.from_array(vals, (2, 2, 0)), b200.allocate(dt, fdom, fill="poison")
-    inner, frame = decomp.split_launches(st.build_info["module"], fdom, (2, 2), {"inp": inp, "out": out},
-                                         {"coeff": 0.05}, native.default_stream(), True)
-    for go in inner + frame:
-        go()
-    native.synchronize(native.default_stream())
-    check(f"hdiff {dt} interior + frame", out.host_array(), oracle.hdiff_c(vals, 0.05))
+    for sides in (True, (False, True, True, False)):  # all four sides; per side (neighbour_sides)
+        out = b200.allocate(dt, fdom, fill="poison")
+        inner, frame = decomp.split_launches(st.build_info["module"], fdom, (2, 2), {"inp": inp, "out": out},
+                                             {"coeff": 0.05}, native.default_stream(), sides)
+        for go in inner + frame:
+            go()
+        native.synchronize(native.default_stream())
+        check(f"hdiff {dt} interior + frame {sides}", out.host_array(), oracle.hdiff_c(vals, 0.05))
 
 # the hdiff tile kernel with mirrored halo stores: 8 boxes into a scratch field
 hdom = (37, 300, 3)
