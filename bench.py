@@ -611,6 +611,14 @@ def c4_weak_scaling(dist, args, tile=(512, 1024, 80)):
     if dist.world == 1:  # the fused step's kernel (mirror build, no neighbours) as one launch
         ms_f, _, _, lps_f = decomposed_hdiff(dist, nst, args.warmup, tile=tile, transport="fused")
         out["fused_us"] = ms_f * 1e3
+        # all 8 ranks of the 4x2 grid (north_star's 8-GPU layout) as virtual
+        # ranks on this GPU (concurrent kernels)
+        try:
+            loc = c4_local_group((4, 2), tile, steps=20)
+            loc["work_ratio"] = loc["ranks"] * out["tile_us"] / loc["us_per_step"]
+            out["local_4x2"] = loc
+        except Exception as exc:  # reported, not fatal
+            out["local_4x2"] = {"error": f"{type(exc).__name__}: {exc}"[:200]}
     for tr in transports:
         try:
             ms, gdom, grid, lps = decomposed_hdiff(dist, nst, args.warmup, tile=tile, transport=tr)
@@ -620,6 +628,59 @@ def c4_weak_scaling(dist, args, tile=(512, 1024, 80)):
         except Exception as exc:  # reported, not fatal
             out[tr] = {"error": f"{type(exc).__name__}: {exc}"[:200]}
     return out
+
+
+def c4_local_group(grid=(2, 2), tile=(512, 1024, 80), steps=20) -> dict:
+    """The fused C4 step (hdiff ping-pong, halo exchange fused into the tile
+    kernel) with every rank of a ``grid`` decomposition as a virtual rank of
+    this process on one GPU, each on its own stream
+    (decomp.PeerFusedStep.local_group): all ranks' ``steps``-step graphs
+    launched together, timed from one event before to the join after.  The
+    ranks share the GPU, so ``work_ratio`` = ranks x the tile alone / the
+    step time measures what the protocol (flags, mirror stores into each
+    other's halos) costs with the kernels really concurrent -- not scaling."""
+    import paper_2311_08322_b200 as b200
+    from paper_2311_08322_b200 import decomp, native, workloads
+
+    nr = grid[0] * grid[1]
+    gdom = (tile[0] * grid[0], tile[1] * grid[1], tile[2])
+    st = b200.compile_stencil(workloads.source("hdiff"), "hdiff", gen_options={"mirror": "out"})
+    ds = [decomp.Decomposition(gdom, grid, r) for r in range(nr)]
+    phases = []
+    for r, d in enumerate(ds):
+        vals = np.random.default_rng(3000 + r).uniform(-1, 1, (tile[0] + 4, tile[1] + 4, tile[2]))
+        A, B = b200.from_array(vals, (2, 2, 0)), b200.from_array(vals, (2, 2, 0))
+        phases.append([{"inp": A, "out": B}, {"inp": B, "out": A}])
+    streams = [native.aux_stream(f"vrank{r}") for r in range(nr)]
+    group = decomp.PeerFusedStep.local_group(st, ds, phases, {"coeff": 0.05}, "out", (2, 2), streams)
+    for _ in range(4):
+        for s_ in group:
+            s_()
+    graphs = [s_.graph(steps) for s_ in group]
+    master = native.default_stream()
+
+    def replay() -> float:
+        e0, e1 = native.Event(), native.Event()
+        for s_ in group:
+            native.synchronize(s_.stream)
+        e0.record(master)
+        for s_ in group:
+            native.call("gts_b200_stream_wait_event", s_.stream, e0.ptr)
+        for g in graphs:
+            g.launch()
+        ends = []
+        for s_ in group:
+            ev = native.Event()
+            ev.record(s_.stream)
+            native.call("gts_b200_stream_wait_event", master, ev.ptr)
+            ends.append(ev)
+        e1.record(master)
+        native.synchronize(master)
+        return e0.elapsed_ms(e1) / steps
+
+    replay()
+    ms = min(replay() for _ in range(3))
+    return {"grid": list(grid), "ranks": nr, "us_per_step": ms * 1e3}
 
 
 def dycore_decomposed_peer(dist, steps=20, tile=(512, 512, 80)):

@@ -719,11 +719,46 @@ class PeerFusedStep:
     read)."""
 
     def __init__(self, stencil, decomposition: Decomposition, phases: list, scalars: dict,
-                 out_field: str, halo: tuple, group=None, stream: Optional[int] = None):
+                 out_field: str, halo: tuple, group=None, stream: Optional[int] = None, _local=False):
         import ctypes
 
+        from . import native
+
+        self._prepare(stencil, decomposition, phases, scalars, out_field, halo, stream)
+        if _local:  # PeerFusedStep.local_group connects the virtual ranks itself
+            return
         import torch.distributed as dist
 
+        single = tuple(decomposition.grid) == (1, 1)  # no neighbours, no process group needed
+        allv = []
+        if not single:
+            def handle(ptr):
+                h, off = ctypes.create_string_buffer(64), ctypes.c_size_t()
+                native.call("gts_b200_ipc_get_handle", ptr, h, ctypes.byref(off))
+                return h.raw, off.value
+
+            me = {"outs": [(handle(f.base_address()), tuple(f.strides), tuple(f.origin)) for f in self._outs],
+                  "flags": handle(self._flags.dptr), "box": (decomposition.i0, decomposition.j0)}
+            allv = [None] * dist.get_world_size(group)
+            dist.all_gather_object(allv, me, group=group)
+
+        def ipc_open(h):
+            p = ctypes.c_void_p()
+            native.call("gts_b200_ipc_open", h, ctypes.byref(p))
+            self._opened.append(p.value)
+            return p.value
+
+        self._connect(allv, ipc_open)
+        if not single:
+            dist.barrier(group)  # every rank mapped its peers
+            # the initial halos are valid and no buffer is being read: one
+            # arrival per neighbour lets everyone's first step start
+            native.call("gts_b200_flags_add", self._remote_arr, self._n, self.stream)
+            native.synchronize(self.stream)
+            dist.barrier(group)
+
+    def _prepare(self, stencil, decomposition, phases, scalars, out_field, halo, stream) -> None:
+        """This rank's own state: flags, expected counts, its output storages."""
         from . import native, storage
 
         module = stencil.build_info["module"]
@@ -733,13 +768,12 @@ class PeerFusedStep:
         self.stream = native.default_stream() if stream is None else stream
         self.phases = phases
         self.out_field = out_field
-        dom = decomposition.local_domain
+        self._scalars, self._halo = scalars, halo
         self._flags = storage._DeviceBuffer(64, pinned_host=False)  # ARRIVED[8], one per direction
         self._expect = storage._DeviceBuffer(64, pinned_host=False)
         native.call("gts_b200_memset", self._flags.dptr, 0, 64, self.stream)
         native.call("gts_b200_memset", self._expect.dptr, 0, 64, self.stream)
         native.synchronize(self.stream)
-
         outs = []  # distinct output storages across phases, shared with the neighbours
         for ph in phases:
             f = ph[out_field]
@@ -747,59 +781,68 @@ class PeerFusedStep:
                 raise TypeError("PeerFusedStep needs DeviceFieldStorages")
             if all(f is not o for o in outs):
                 outs.append(f)
-
-        def handle(ptr):
-            h, off = ctypes.create_string_buffer(64), ctypes.c_size_t()
-            native.call("gts_b200_ipc_get_handle", ptr, h, ctypes.byref(off))
-            return h.raw, off.value
-
+        self._outs = outs
         self._opened = []
-        self.neighbours = mirror_boxes(decomposition, halo)
-        single = tuple(decomposition.grid) == (1, 1)  # no neighbours, no process group needed
-        allv = []
-        if not single:
-            me = {"outs": [(handle(f.base_address()), tuple(f.strides), tuple(f.origin)) for f in outs],
-                  "flags": handle(self._flags.dptr), "box": (decomposition.i0, decomposition.j0)}
-            allv = [None] * dist.get_world_size(group)
-            dist.all_gather_object(allv, me, group=group)
+
+    def _connect(self, allv: list, open_fn) -> None:
+        """Map every neighbour's flags and outputs (``allv[rank]``: its
+        ``outs`` / ``flags`` handles and box origin; ``open_fn`` turns a
+        handle into a device pointer: CUDA IPC between processes, the
+        pointer itself within one) and build the per-phase mirror boxes and
+        launchers."""
+        import ctypes
+
+        decomposition, module = self.decomp, self.module
+        dom = decomposition.local_domain
+        self.neighbours = mirror_boxes(decomposition, self._halo)
         remote_outs, self._remote_flags, self._my_flags = {}, [], []
         for d, nb, box in self.neighbours:
             info = allv[nb]
-            gp = ctypes.c_void_p()
-            native.call("gts_b200_ipc_open", info["flags"][0], ctypes.byref(gp))
-            self._opened.append(gp.value)
+            gp = open_fn(info["flags"][0])
             opp = DIRS8.index(tuple(-x for x in DIRS8[d]))
-            self._remote_flags.append(gp.value + info["flags"][1] + 8 * opp)
+            self._remote_flags.append(gp + info["flags"][1] + 8 * opp)
             self._my_flags.append(self._flags.dptr + 8 * d)
             for oi, ((h, off), strides, origin) in enumerate(info["outs"]):
-                fp = ctypes.c_void_p()
-                native.call("gts_b200_ipc_open", h, ctypes.byref(fp))
-                self._opened.append(fp.value)
-                remote_outs[(d, oi)] = (fp.value + off, strides, origin, info["box"])
+                remote_outs[(d, oi)] = (open_fn(h) + off, strides, origin, info["box"])
         n = len(self.neighbours)
         self._n = n
         self._remote_arr = (ctypes.c_void_p * max(1, n))(*self._remote_flags)
         self._my_arr = (ctypes.c_void_p * max(1, n))(*self._my_flags)
         # per phase: the mirror boxes into the neighbours' copy of that phase's output
         self._boxes, self._launch = [], []
-        item = outs[0].itemsize
-        for ph in phases:
-            oi = next(x for x, f in enumerate(outs) if f is ph[out_field])
+        item = self._outs[0].itemsize
+        for ph in self.phases:
+            oi = next(x for x, f in enumerate(self._outs) if f is ph[self.out_field])
             boxes = []
             for d, nb, box in self.neighbours:
                 base, strides, origin, _ = remote_outs[(d, oi)]
                 nbd = Decomposition(decomposition.global_domain, decomposition.grid, nb)
                 boxes.append(mirror_descriptor(decomposition, nbd, box, base, strides, origin, item))
             self._boxes.append(boxes)
-            self._launch.append(module.launcher(dom, ph, scalars, self.stream))
+            self._launch.append(module.launcher(dom, ph, self._scalars, self.stream))
         self._step = 0
-        if not single:
-            dist.barrier(group)  # every rank mapped its peers
-            # the initial halos are valid and no buffer is being read: one
-            # arrival per neighbour lets everyone's first step start
-            native.call("gts_b200_flags_add", self._remote_arr, n, self.stream)
-            native.synchronize(self.stream)
-            dist.barrier(group)
+
+    @classmethod
+    def local_group(cls, stencil, decompositions: list, phases: list, scalars: dict, out_field: str,
+                    halo: tuple, streams: list) -> list:
+        """All ranks of a decomposition as virtual ranks of ONE process on one
+        GPU, each on its own stream (``phases[r]``, ``streams[r]``): the same
+        kernels, mirror stores and step flags as across GPUs, with the
+        neighbours' outputs and flags addressed directly instead of through
+        CUDA IPC.  The ranks' kernels run concurrently (no context
+        time-slicing), so the step time shows the protocol's cost on
+        hardware; it is not a scaling number (the ranks share one GPU)."""
+        steps = [cls(stencil, d, ph, scalars, out_field, halo, stream=st, _local=True)
+                 for d, ph, st in zip(decompositions, phases, streams)]
+        allv = [{"outs": [((f.base_address(), 0), tuple(f.strides), tuple(f.origin)) for f in s_._outs],
+                 "flags": (s_._flags.dptr, 0), "box": (s_.decomp.i0, s_.decomp.j0)} for s_ in steps]
+        for s_ in steps:
+            s_._connect(allv, lambda h: h)
+        for s_ in steps:
+            s_.native.call("gts_b200_flags_add", s_._remote_arr, s_._n, s_.stream)
+        for s_ in steps:
+            s_.native.synchronize(s_.stream)
+        return steps
 
     def __call__(self) -> None:
         p = self._step % len(self.phases)

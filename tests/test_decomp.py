@@ -626,3 +626,67 @@ def test_hdiff_mirror_stores_exact_cells_single_process():
     st_m(inp=inp, coeff=0.05, out=out)
     scratch.mark_device_written()
     assert np.all(scratch.host_array() == -9.0)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kernel", ["hdiff", "dycore"])
+@pytest.mark.parametrize("grid", [(2, 1), (2, 2), (4, 2)])
+def test_peer_fused_local_group_bitwise(kernel, grid):
+    """PeerFusedStep.local_group: every rank of the decomposition as a virtual
+    rank of this process, each on its own stream, all enqueued before any is
+    synchronised (the ranks' kernels, mirror stores into each other's halos
+    and step flags run concurrently on the GPU, no host ordering between
+    them): 5 eager steps and two replays of a 2-step CUDA graph per rank,
+    every rank's block bitwise equal to the undecomposed oracle run."""
+    import numpy as np
+
+    import oracle
+    import paper_2311_08322_b200 as b200
+    from paper_2311_08322_b200 import decomp, native, workloads
+
+    if kernel == "hdiff":
+        gdom = (37 * grid[0] + 3, 140 * grid[1] + 5, 6)
+        arr = {"u": np.random.default_rng(11).uniform(-1, 1, (gdom[0] + 4, gdom[1] + 4, gdom[2]))}
+        sc, fin, fout = {"coeff": 0.05}, "inp", "out"
+        run = lambda n: oracle.hdiff_run(arr["u"], n, 0.05)  # noqa: E731
+    else:
+        gdom = (37 * grid[0] + 3, 70 * grid[1] + 5, 16)
+        arr = workloads.dycore_arrays(gdom, 11)
+        sc, fin, fout = workloads.DYCORE_SCALARS, "u_in", "u_out"
+        run = lambda n: oracle.dycore_run(arr["u"], arr["a"], arr["b"], arr["c"], n, **sc)  # noqa: E731
+    st = b200.compile_stencil(workloads.source(kernel), kernel, gen_options={"mirror": fout})
+    nr = grid[0] * grid[1]
+    ds = [decomp.Decomposition(gdom, grid, r) for r in range(nr)]
+    bufs, phases = [], []
+    for d in ds:
+        u = d.scatter(arr["u"], (2, 2))
+        coef = {} if kernel == "hdiff" else {
+            n: b200.from_array(np.array(arr[n][d.i0: d.i1, d.j0: d.j1, :], copy=True)) for n in "abc"}
+        A, B = b200.from_array(u, (2, 2, 0)), b200.from_array(u, (2, 2, 0))
+        bufs.append((A, B))
+        phases.append([{fin: A, fout: B, **coef}, {fin: B, fout: A, **coef}])
+    streams = [native.aux_stream(f"vrank{r}") for r in range(nr)]
+    steps = decomp.PeerFusedStep.local_group(st, ds, phases, sc, fout, (2, 2), streams)
+
+    def check(n, which):
+        want = run(n)[2:-2, 2:-2, :]
+        for d, (A, B) in zip(ds, bufs):
+            got = (B if which else A).host_array()[2:-2, 2:-2, :]
+            assert np.array_equal(got, want[d.i0: d.i1, d.j0: d.j1, :]), (kernel, grid, n, d.rank)
+
+    for _ in range(5):
+        for s_ in steps:
+            s_()
+    for s_ in steps:
+        native.synchronize(s_.stream)
+    check(5, 1)
+    # one more step to phase 0, then graph replays (2 steps each, all ranks' graphs launched together)
+    for s_ in steps:
+        s_()
+    graphs = [s_.graph(2) for s_ in steps]
+    for _ in range(2):
+        for g in graphs:
+            g.launch()
+    for s_ in steps:
+        native.synchronize(s_.stream)
+    check(10, 0)
