@@ -630,7 +630,7 @@ def c4_weak_scaling(dist, args, tile=(512, 1024, 80)):
     return out
 
 
-def c4_local_group(grid=(2, 2), tile=(512, 1024, 80), steps=20) -> dict:
+def c4_local_group(grid=(2, 2), tile=(512, 1024, 80), steps=20, kernel="hdiff") -> dict:
     """The fused C4 step (hdiff ping-pong, halo exchange fused into the tile
     kernel) with every rank of a ``grid`` decomposition as a virtual rank of
     this process on one GPU, each on its own stream
@@ -644,15 +644,21 @@ def c4_local_group(grid=(2, 2), tile=(512, 1024, 80), steps=20) -> dict:
 
     nr = grid[0] * grid[1]
     gdom = (tile[0] * grid[0], tile[1] * grid[1], tile[2])
-    st = b200.compile_stencil(workloads.source("hdiff"), "hdiff", gen_options={"mirror": "out"})
+    fin, fout = ("inp", "out") if kernel == "hdiff" else ("u_in", "u_out")
+    sc = {"coeff": 0.05} if kernel == "hdiff" else workloads.DYCORE_SCALARS
+    st = b200.compile_stencil(workloads.source(kernel), kernel, gen_options={"mirror": fout})
     ds = [decomp.Decomposition(gdom, grid, r) for r in range(nr)]
     phases = []
     for r, d in enumerate(ds):
-        vals = np.random.default_rng(3000 + r).uniform(-1, 1, (tile[0] + 4, tile[1] + 4, tile[2]))
+        if kernel == "hdiff":
+            vals, coef = np.random.default_rng(3000 + r).uniform(-1, 1, (tile[0] + 4, tile[1] + 4, tile[2])), {}
+        else:
+            arr = workloads.dycore_arrays(d.local_domain, 3000 + r)
+            vals, coef = arr["u"], {n: b200.from_array(arr[n]) for n in "abc"}
         A, B = b200.from_array(vals, (2, 2, 0)), b200.from_array(vals, (2, 2, 0))
-        phases.append([{"inp": A, "out": B}, {"inp": B, "out": A}])
+        phases.append([{fin: A, fout: B, **coef}, {fin: B, fout: A, **coef}])
     streams = [native.aux_stream(f"vrank{r}") for r in range(nr)]
-    group = decomp.PeerFusedStep.local_group(st, ds, phases, {"coeff": 0.05}, "out", (2, 2), streams)
+    group = decomp.PeerFusedStep.local_group(st, ds, phases, sc, fout, (2, 2), streams)
     for _ in range(4):
         for s_ in group:
             s_()
@@ -983,6 +989,11 @@ def run_b200(args, dist):
             dy["frac"] = dy.pop("achieved_gbs") / peak
         extra["dycore"] = dy
         extra["dycore_fused_peer"] = _extra_guard(dycore_fused_peer, dist)
+        # the fused dycore step on all 4 ranks of a 2x2 grid as virtual ranks (concurrent kernels)
+        dl = _extra_guard(c4_local_group, (2, 2), (512, 512, 80), 20, "dycore")
+        if "us_per_step" in dl and "us_per_step" in dy:
+            dl["work_ratio"] = dl["ranks"] * dy["us_per_step"] / dl["us_per_step"]
+        extra["dycore_fused_local_2x2"] = dl
     if dist.world > 1 and not args.no_extra:
         extra["dycore_decomposed_peer"] = _extra_guard(dycore_decomposed_peer, dist)
         extra["dycore_fused_peer"] = _extra_guard(dycore_fused_peer, dist)
