@@ -403,8 +403,10 @@ class _Pipeline:
     # vadv 3.65 / 3.79 / 3.62 / 3.67 ms and hdiff 1.55 / 1.48 / 1.38 / 1.42 ms
     # per call at 16 / 32 / 64 / 128 rows; a concurrent 2-D device->host copy
     # slows the host->device stream (0.4 ms at 32 rows), less so with fewer,
-    # larger segments
-    CHUNK_ROWS = 64
+    # larger segments.  Round 2 (tapered, medians of 3): vadv 3.60 / 3.54 / 3.52
+    # ms and hdiff 1.383 / 1.386 / 1.461 ms at 64 / 96 / 128 rows
+    CHUNK_ROWS = 96
+    MIN_ROWS = 128  # fewer i rows: one unpipelined copy-in / launch / copy-out
 
     # shrink the last chunks (shorter kernel + D2H tail after the last upload):
     # measured vadv 256^2x80 3.62 -> 3.58 ms per call, hdiff unchanged (1.37)
@@ -440,7 +442,7 @@ class _Pipeline:
         self.ext = {n: impl.field_extent(n) for n in module.field_order}
 
     def eligible(self, domain, field_args) -> bool:
-        if domain[0] < 2 * self.CHUNK_ROWS:
+        if domain[0] < self.MIN_ROWS:
             return False
         if not all(_call_local(self.impl, n, domain[2]) for n in self.read_outputs):
             return False
