@@ -583,7 +583,7 @@ def _time_replay(dist, replay, stream, steps, step) -> float:
     return ms
 
 
-def c4_weak_scaling(dist, args, tile=(512, 1024, 80)):
+def c4_weak_scaling(dist, args, tile=(512, 1024, 80), out=None):
     """BASELINE configs[3] / north_star scaling target: hdiff f64 with a fixed
     512x1024x80 tile per GPU on the rank grid (1x1, 2x1, 2x2, 4x2 -> 2048x
     2048x80 at 8 GPUs).  Measured in this run: the tile alone (no neighbours,
@@ -591,7 +591,10 @@ def c4_weak_scaling(dist, args, tile=(512, 1024, 80)):
     and (N > 1) the peer-memory transport; efficiency = tile time / step time
     (weak scaling, max over ranks)."""
     nst = max(args.steps // 4, 20)
-    out: dict = {"tile": list(tile), "gpus": dist.world}
+    # filled in place: a caller that already holds ``out`` (the JSON line at
+    # N > 1) keeps every number measured before a later transport hangs
+    out = {} if out is None else out
+    out.update({"tile": list(tile), "gpus": dist.world})
     ms1, _, _, lps1 = decomposed_hdiff(dist, nst, args.warmup, tile=tile, transport="none")
     out["tile_us"] = ms1 * 1e3
     out["tile_launches_per_step"] = lps1
@@ -948,17 +951,27 @@ def run_b200(args, dist):
         if not done.wait(args.extra_timeout):
             if dist.rank == 0:
                 line["extra"] = {"error": f"extras timed out after {args.extra_timeout:.0f} s"}
-                print(json.dumps(_r(line)), flush=True)
+                text = None
+                for _ in range(5):  # the main thread may still be filling line["c4"]
+                    try:
+                        text = json.dumps(_r(line))
+                        break
+                    except RuntimeError:
+                        time.sleep(0.05)
+                if text is None:
+                    text = json.dumps(_r({k: v for k, v in line.items() if k != "c4"}))
+                print(text, flush=True)
             os._exit(0)
 
     threading.Thread(target=_watchdog, daemon=True).start()
     extra: dict = {}
     if not args.no_extra:
-        c4 = c4_weak_scaling(dist, args)
-        detail["c4"] = c4
+        c4: dict = {}
         if dist.world > 1:
-            line["c4"] = c4
-        else:
+            line["c4"] = c4  # the watchdog's line keeps what was measured before a hang
+        c4_weak_scaling(dist, args, out=c4)
+        detail["c4"] = c4
+        if dist.world == 1:
             extra["c4_tile"] = c4
     if dist.rank == 0 and dist.world == 1 and not args.no_extra:
         nst = max(args.steps // 2, 50)
