@@ -869,6 +869,21 @@ def conversion_roofline(st, domain, seconds, sampler):
             "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "Tconv/s", "frac": achieved / peak}
 
 
+def compact_line(line: dict) -> dict:
+    """The JSON line as printed: the N > 1 ``c4`` block without the fields
+    the rest derive (launch counts, global domain, per-transport value)."""
+    out = dict(line)
+    c4 = out.get("c4")
+    if isinstance(c4, dict):
+        c = {k: v for k, v in c4.items()
+             if k not in ("tile_launches_per_step", "split_launches_per_step", "global", "split_us")}
+        for tr in ("nccl", "peer", "fused"):
+            if isinstance(c.get(tr), dict):
+                c[tr] = {k: v for k, v in c[tr].items() if k != "value"}
+        out["c4"] = c
+    return out
+
+
 def compact_extra(extra: dict) -> dict:
     """The extras as they go on the JSON line (the driver keeps a 1500-char
     stdout tail): times and fractions only, parity "bitwise" meaning equal
@@ -994,7 +1009,7 @@ def run_b200(args, dist):
                 text = None
                 for _ in range(5):  # the main thread may still be filling line["c4"]
                     try:
-                        text = json.dumps(_r(line))
+                        text = json.dumps(_r(compact_line(line)))
                         break
                     except RuntimeError:
                         time.sleep(0.05)
@@ -1073,7 +1088,7 @@ def run_b200(args, dist):
             _detail_path(dist).write_text(json.dumps(detail, indent=1, default=str))
         except OSError:
             pass
-        print(json.dumps(_r(line)), flush=True)
+        print(json.dumps(_r(compact_line(line))), flush=True)
 
 
 def main():
