@@ -292,8 +292,9 @@ FRAME = False  # frame variant: the launch enumerates only the tiles outside an 
 FASTDIV = True  # tile index division by multiply-high (gts_div_c) instead of the XU-pipe division
 MIRROR = None  # gen_options mirror: the buffered api output also stored into neighbour halo boxes
 L2PF0 = 0  # gen_options pf_l2pf0: with PDL, this many of the CTA's first tiles prefetched into L2 before the wait
+TMAST = False  # gen_options pf_tmastore: outputs staged per warp strip and written by one TMA bulk store
 DEFAULTS = {"pf_nw": 4, "pf_ri": 8, "pf_vj": 4, "pf_nbuf": 1, "pf_prefetch": 0, "pf_swz": 0, "pf_pdl": "off",
-            "pf_frame": 0, "pf_fastdiv": 1, "pf_l2pf0": 0}
+            "pf_frame": 0, "pf_fastdiv": 1, "pf_l2pf0": 0, "pf_tmastore": 0}
 # Measured defaults per element size (profiles/sweep_hdiff_r1.md, hdiff
 # 256x256x80 on one B200, CUDA-graph timed):
 #  f64: 16x128 tiles, double-buffered TMA boxes: 16.9 us vs 18.1 us for
@@ -317,8 +318,11 @@ DEFAULTS = {"pf_nw": 4, "pf_ri": 8, "pf_vj": 4, "pf_nbuf": 1, "pf_prefetch": 0, 
 #       tail; tools/abtest.py, medians of 5): f64 256^2 15.70 -> 14.93 us (2 tiles:
 #       16.52), 512x1024 112.6 -> 112.1; f32 with late PDL 15.09 -> 13.72 us
 #       (late PDL alone 15.12, 2 tiles 14.62).
+#  pf_tmastore (round 2; each warp stages its strip's output rows in shared
+#       memory and writes them with one TMA bulk tensor store per tile): f64 256^2
+#       14.97 -> 14.36 us, 512x1024 112.9 -> 108.5 us; f32 13.72 -> 15.26 us (off).
 GEOMETRY = {8: {"pf_nw": 2, "pf_ri": 4, "pf_vj": 4, "pf_nbuf": 2, "pf_prefetch": 1, "pf_swz": 1,
-                "pf_pdl": "late", "pf_fastdiv": 1, "pf_l2pf0": 1},
+                "pf_pdl": "late", "pf_fastdiv": 1, "pf_l2pf0": 1, "pf_tmastore": 1},
             4: {"pf_nw": 2, "pf_ri": 8, "pf_vj": 4, "pf_nbuf": 2, "pf_prefetch": 1, "pf_swz": 0,
                 "pf_pdl": "late", "pf_fastdiv": 0, "pf_l2pf0": 1}}
 
@@ -331,7 +335,7 @@ LARGE = {"pf_nw": 4}
 LARGE_POINTS = 16 * 1024 * 1024
 # Tiny binary64 domains (< TINY_POINTS) use 2-row strips: 128^2x64 5.97 -> 5.58 us,
 # but 192^2x80 12.54 -> 14.10 us (tools/abtest.py).
-TINY = {"pf_ri": 2}
+TINY = {"pf_ri": 2, "pf_tmastore": 0}  # bulk stores: 128^2x64 4.98 -> 5.07 us, so row stores there
 TINY_POINTS = 2 * 1024 * 1024
 # The frame launch of a decomposed step (decomp.DecomposedStep): after the
 # halo exchange, only the tiles that touch the halo-dependent band run, in
@@ -351,7 +355,7 @@ def configure(opts, esize: int = 0) -> None:
     fingerprint like the reference gen engine's tile options, gen.py:235-238).
     Unset options take the measured default of the group's smallest streamed
     element size ``esize`` (0: the generic DEFAULTS)."""
-    global NW, RI, VJ, TJ, TI, NBUF, PREFETCH, SWZ, PDL, FRAME, FASTDIV, L2PF0
+    global NW, RI, VJ, TJ, TI, NBUF, PREFETCH, SWZ, PDL, FRAME, FASTDIV, L2PF0, TMAST
     o = dict(DEFAULTS)
     o.update(GEOMETRY.get(esize, {}))
     o.update({k: v for k, v in (opts or {}).items() if k in DEFAULTS})
@@ -362,6 +366,7 @@ def configure(opts, esize: int = 0) -> None:
     FRAME = bool(int(o["pf_frame"]))
     FASTDIV = bool(int(o["pf_fastdiv"]))
     L2PF0 = int(o["pf_l2pf0"])
+    TMAST = bool(int(o["pf_tmastore"]))
     TJ, TI = 32 * VJ, NW * RI
 
 
@@ -395,13 +400,27 @@ def emit(kname: str, plan, kplan, ctype: dict, dtypes: dict, opts=None):
     tm = ", ".join(f"const __grid_constant__ CUtensorMap tm_{s.name}" for s in streams)
     smem = NBUF * geo.buf_bytes
     bar_off = smem
+    # gen_options pf_tmastore: each warp stages its strip's rows of the buffered
+    # api outputs in shared memory and stores them with ONE TMA bulk tensor
+    # store per tile (cp.async.bulk.tensor ... bulk_group) instead of per-row STG
+    tmast = TMAST and not FRAME and MIRROR is None and len(geo.buffered) > 0
+    stg_off, stg_bytes = {}, {}
+    if tmast:
+        o = -(-(bar_off + 16) // 128) * 128
+        for f in sorted(geo.buffered):
+            e = 8 if dtypes[f] == ir.F64 else 4
+            stg_off[f], stg_bytes[f] = o, RI * TJ * e  # per warp
+            o += NW * RI * TJ * e
+        smem = o - 16  # smem_bytes below adds the barrier slot back
     w(f"// fused PARALLEL tile kernel: {TI}x{TJ} tile per k-plane, {NW} warps x {RI} rows, "
       f"{VJ} columns/lane; streamed {[s.name for s in streams]}, register windows "
       f"{[(x.name, x.rlo, x.rhi, x.clo, x.chi) for x in regw]}")
     minb = int((opts or {}).get("pf_minb", 0))  # min resident CTAs/SM (register cap), 0 = compiler's choice
     lb = f"{32 * NW}, {minb}" if minb else f"{32 * NW}"
     frame_args = ", int fi0, int fi1, int fj0, int fj1" if FRAME else ", GtsFastDiv dvp, GtsFastDiv dvj"
-    w(f"__global__ void __launch_bounds__({lb}) {kname}(const __grid_constant__ GtsParams p, {tm}, "
+    tmo = ("".join(f", const __grid_constant__ CUtensorMap tmo_{f}" for f in sorted(geo.buffered)) + ", int tmo_on"
+           if tmast else "")
+    w(f"__global__ void __launch_bounds__({lb}) {kname}(const __grid_constant__ GtsParams p, {tm}{tmo}, "
       f"int k0, int nkr, int tiles_i, int tiles_j, int ntiles{frame_args}) {{")
     w("  extern __shared__ __align__(1024) unsigned char smem[];")
     w(f"  uint64_t* full = (uint64_t*)(smem + {bar_off});")
@@ -619,6 +638,12 @@ def emit(kname: str, plan, kplan, ctype: dict, dtypes: dict, opts=None):
             assign(c, v, "q_")
             w("      }")
 
+    if tmast:
+        # the warp's staging tile is free once its previous bulk store has read it
+        w('    if (tmo_on && lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");')
+        w("    __syncwarp();")
+        for f in sorted(geo.buffered):
+            w(f"    {ctype[f]}* const stg_{f} = ({ctype[f]}*)(smem + {stg_off[f]} + warp * {stg_bytes[f]});")
     # fully unrolled steps (prologue + main)
     for step in range(nsteps):
         rel = steps_lo + step  # r = ra + rel
@@ -659,6 +684,20 @@ def emit(kname: str, plan, kplan, ctype: dict, dtypes: dict, opts=None):
                 _emit_point(st.body, ctx, ctype, api, out, "          ", local, geo)
                 w("        }")
             w("      }")
+        if rel >= 0 and pf_debug != "streamonly" and tmast:
+            # staged rows: the strip leaves as one TMA bulk store after the steps
+            w("      if (tmo_on) {")
+            for f in sorted(geo.buffered):
+                e = 8 if dtypes[f] == ir.F64 else 4
+                if e == 8:
+                    for q in range(0, VJ, 2):
+                        w(f"      *reinterpret_cast<double2*>(stg_{f} + {rel * TJ} + lane * {VJ} + {q}) = "
+                          f"make_double2(o_{f}[{q}], o_{f}[{q + 1}]);")
+                else:
+                    for q in range(0, VJ, 4):
+                        w(f"      *reinterpret_cast<float4*>(stg_{f} + {rel * TJ} + lane * {VJ} + {q}) = "
+                          f"make_float4(o_{f}[{q}], o_{f}[{q + 1}], o_{f}[{q + 2}], o_{f}[{q + 3}]);")
+            w("      } else {")  # no store map for this layout: the row stores below
         if rel >= 0 and pf_debug != "streamonly":
             # buffered api outputs: one row of VJ values per lane, vector store
             for f in sorted(geo.buffered):
@@ -704,9 +743,25 @@ def emit(kname: str, plan, kplan, ctype: dict, dtypes: dict, opts=None):
                     w("          }")
                     w("        }")
                 w("      }")
+            if tmast:
+                w("      }")
+        w("    }")
+    if tmast:
+        w("    if (tmo_on) {")
+        w('    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the staged rows, to the TMA engine')
+        w("    __syncwarp();")
+        w("    if (lane == 0) {")
+        for f in sorted(geo.buffered):
+            w(f'      asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {{%1, %2, %3}}], [%4];"'
+              f' :: "l"(reinterpret_cast<uint64_t>(&tmo_{f})), "r"(j0), "r"(ra), "r"(kk),'
+              f' "r"(gts_smem_u32(stg_{f})) : "memory");')
+        w('      asm volatile("cp.async.bulk.commit_group;" ::: "memory");')
+        w("    }")
         w("    }")
     w("    __syncthreads();  // both buffers' readers done before the next prefetch reuses this one")
     w("  }")
+    if tmast:
+        w('  if (tmo_on && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");')
     w("}")
 
     smem_bytes = smem + 16
@@ -725,6 +780,19 @@ def emit(kname: str, plan, kplan, ctype: dict, dtypes: dict, opts=None):
             f" {s.box_cols}, {s.box_rows}, 1);",
         ]
     tm_args = ", ".join(f"tm_{kname}_{s.name}" for s in streams)
+    if tmast:
+        # store maps: the output's compute domain at its origin, box = one warp's strip
+        for f in sorted(geo.buffered):
+            e = 8 if dtypes[f] == ir.F64 else 4
+            pre += [
+                f"  CUtensorMap tmo_{kname}_{f};",
+                f"  memset(&tmo_{kname}_{f}, 0, sizeof(CUtensorMap));",
+                f"  const bool tmok_{kname}_{f} = gts_make_tmap_3d(&tmo_{kname}_{f}, (const void*)&GTS_AT(p.f_{f}, 0, 0, 0),"
+                f" {e}, nj, ni, nk, p.f_{f}.si, p.f_{f}.sj, p.f_{f}.sk, {TJ}, {RI}, 1);",
+            ]
+        # a layout without a valid store map (16-B alignment) keeps the row stores
+        tm_args += "".join(f", tmo_{kname}_{f}" for f in sorted(geo.buffered))
+        tm_args += ", (int)(" + " && ".join(f"tmok_{kname}_{f}" for f in sorted(geo.buffered)) + ")"
     if FRAME:
         # inner tile rectangle: tiles whose points all lie at least the band
         # width of their side inside the domain (they need no halo cell of a
