@@ -403,7 +403,7 @@ def emit(kname: str, plan, kplan, ctype: dict, dtypes: dict, opts=None):
     # gen_options pf_tmastore: each warp stages its strip's rows of the buffered
     # api outputs in shared memory and stores them with ONE TMA bulk tensor
     # store per tile (cp.async.bulk.tensor ... bulk_group) instead of per-row STG
-    tmast = TMAST and not FRAME and MIRROR is None and len(geo.buffered) > 0
+    tmast = TMAST and not FRAME and len(geo.buffered) > 0
     stg_off, stg_bytes = {}, {}
     if tmast:
         o = -(-(bar_off + 16) // 128) * 128
@@ -638,6 +638,30 @@ def emit(kname: str, plan, kplan, ctype: dict, dtypes: dict, opts=None):
             assign(c, v, "q_")
             w("      }")
 
+    def emit_mirror(f):
+        # gen_options mirror: the row's values inside a neighbour's halo
+        # box also go there (peer stores; boundary tiles only)
+        w("        if (nmir_ > 0) {")
+        w("          if (nmir_ <= 3) {")
+        w("            #pragma unroll")
+        w("            for (int m = 0; m < 3; ++m) {")
+        w("              if (m < nmir_ && r >= mi0_[m] && r < mi1_[m] && mcm_[m]) {")
+        w(f"                {ctype[f]}* const mb_ = mbp_[m] + (long long)r * msi_[m];")
+        for q in range(VJ):
+            w(f"                if (mcm_[m] & {1 << q}u) mb_[(long long)(jl + {q}) * msj_[m]] = o_{f}[{q}];")
+        w("              }")
+        w("            }")
+        w("          } else {")
+        w("            for (int d = 0; d < p.mir.n; ++d) {")
+        w("              if (r < p.mir.i0[d] || r >= p.mir.i1[d]) continue;")
+        w(f"              {ctype[f]}* const mb_ = p.mir.base[d] + (long long)r * p.mir.si[d] + (long long)kk * p.mir.sk[d];")
+        for q in range(VJ):
+            w(f"              if (jl + {q} < nj && jl + {q} >= p.mir.j0[d] && jl + {q} < p.mir.j1[d]) "
+              f"mb_[(long long)(jl + {q}) * p.mir.sj[d]] = o_{f}[{q}];")
+        w("            }")
+        w("          }")
+        w("        }")
+
     if tmast:
         # the warp's staging tile is free once its previous bulk store has read it
         w('    if (tmo_on && lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");')
@@ -697,6 +721,10 @@ def emit(kname: str, plan, kplan, ctype: dict, dtypes: dict, opts=None):
                     for q in range(0, VJ, 4):
                         w(f"      *reinterpret_cast<float4*>(stg_{f} + {rel * TJ} + lane * {VJ} + {q}) = "
                           f"make_float4(o_{f}[{q}], o_{f}[{q + 1}], o_{f}[{q + 2}], o_{f}[{q + 3}]);")
+            if MIRROR in geo.buffered:
+                w("      if (r < ni) {")
+                emit_mirror(MIRROR)
+                w("      }")
             w("      } else {")  # no store map for this layout: the row stores below
         if rel >= 0 and pf_debug != "streamonly":
             # buffered api outputs: one row of VJ values per lane, vector store
@@ -720,28 +748,7 @@ def emit(kname: str, plan, kplan, ctype: dict, dtypes: dict, opts=None):
                     w(f"          if (jl + {q} < nj) op[(long long){q} * p.f_{f}.sj] = o_{f}[{q}];")
                 w("        }")
                 if f == MIRROR:
-                    # gen_options mirror: the row's values inside a neighbour's halo
-                    # box also go there (peer stores; boundary tiles only)
-                    w("        if (nmir_ > 0) {")
-                    w("          if (nmir_ <= 3) {")
-                    w("            #pragma unroll")
-                    w("            for (int m = 0; m < 3; ++m) {")
-                    w("              if (m < nmir_ && r >= mi0_[m] && r < mi1_[m] && mcm_[m]) {")
-                    w(f"                {ctype[f]}* const mb_ = mbp_[m] + (long long)r * msi_[m];")
-                    for q in range(VJ):
-                        w(f"                if (mcm_[m] & {1 << q}u) mb_[(long long)(jl + {q}) * msj_[m]] = o_{f}[{q}];")
-                    w("              }")
-                    w("            }")
-                    w("          } else {")
-                    w("            for (int d = 0; d < p.mir.n; ++d) {")
-                    w("              if (r < p.mir.i0[d] || r >= p.mir.i1[d]) continue;")
-                    w(f"              {ctype[f]}* const mb_ = p.mir.base[d] + (long long)r * p.mir.si[d] + (long long)kk * p.mir.sk[d];")
-                    for q in range(VJ):
-                        w(f"              if (jl + {q} < nj && jl + {q} >= p.mir.j0[d] && jl + {q} < p.mir.j1[d]) "
-                          f"mb_[(long long)(jl + {q}) * p.mir.sj[d]] = o_{f}[{q}];")
-                    w("            }")
-                    w("          }")
-                    w("        }")
+                    emit_mirror(f)
                 w("      }")
             if tmast:
                 w("      }")
