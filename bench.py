@@ -618,7 +618,8 @@ def c4_weak_scaling(dist, args, tile=(512, 1024, 80), out=None):
         # ranks on this GPU (concurrent kernels)
         try:
             loc = c4_local_group((4, 2), tile, steps=20)
-            loc["work_ratio"] = loc["ranks"] * out["tile_us"] / loc["us_per_step"]
+            # against the same fused kernel with no neighbours (the protocol's cost)
+            loc["work_ratio"] = loc["ranks"] * out["fused_us"] / loc["us_per_step"]
             out["local_4x2"] = loc
         except Exception as exc:  # reported, not fatal
             out["local_4x2"] = {"error": f"{type(exc).__name__}: {exc}"[:200]}
