@@ -400,18 +400,19 @@ def emit(kname: str, plan, kplan, ctype: dict, dtypes: dict, opts=None):
     tm = ", ".join(f"const __grid_constant__ CUtensorMap tm_{s.name}" for s in streams)
     smem = NBUF * geo.buf_bytes
     bar_off = smem
+    bar_bytes = -(-8 * NBUF // 16) * 16  # the NBUF full barriers
     # gen_options pf_tmastore: each warp stages its strip's rows of the buffered
     # api outputs in shared memory and stores them with ONE TMA bulk tensor
     # store per tile (cp.async.bulk.tensor ... bulk_group) instead of per-row STG
     tmast = TMAST and not FRAME and len(geo.buffered) > 0
     stg_off, stg_bytes = {}, {}
     if tmast:
-        o = -(-(bar_off + 16) // 128) * 128
+        o = -(-(bar_off + bar_bytes) // 128) * 128
         for f in sorted(geo.buffered):
             e = 8 if dtypes[f] == ir.F64 else 4
             stg_off[f], stg_bytes[f] = o, RI * TJ * e  # per warp
             o += NW * RI * TJ * e
-        smem = o - 16  # smem_bytes below adds the barrier slot back
+        smem = o - bar_bytes  # smem_bytes below adds the barrier slot back
     w(f"// fused PARALLEL tile kernel: {TI}x{TJ} tile per k-plane, {NW} warps x {RI} rows, "
       f"{VJ} columns/lane; streamed {[s.name for s in streams]}, register windows "
       f"{[(x.name, x.rlo, x.rhi, x.clo, x.chi) for x in regw]}")
@@ -771,7 +772,7 @@ def emit(kname: str, plan, kplan, ctype: dict, dtypes: dict, opts=None):
         w('  if (tmo_on && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");')
     w("}")
 
-    smem_bytes = smem + 16
+    smem_bytes = smem + bar_bytes
     flag = f"fz_ok_{kname.split('_')[1][1:]}"
     pre = [f"  // TMA maps of {kname}: each covers the field's required region (its extent)"]
     for s in streams:
