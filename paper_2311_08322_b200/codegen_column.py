@@ -540,15 +540,14 @@ def _emit_variant(kname, plan, sp: ThomasSpec, v: Variant, ctype, dtypes, opts):
     # round is bandwidth-bound either way) and +1% where no split applies
     # (the runtime level stride), so it is opt-in
     split = not v.hbox and not v.mat and bool((opts or {}).get("col_split", False))
-    # gen_options col_l2pf: L2 prefetch of the next tile's first col_l2pf ring
-    # stages beyond the ring, issued col_l2pf_d stages before this tile's last
-    # stage; col_l2pf0: the first tile's first stages before griddepcontrol.wait
+    # gen_options col_l2pf: in two-round grids, L2 prefetch of a CTA's second
+    # tile's next col_l2pf stages once the ring holds its first ones;
+    # col_l2pf0: the first tile's first stages before griddepcontrol.wait.
     # Measured (tools/abtest.py, medians of 5): vadv 256^2 36.66 -> 35.56 us with
-    # 8 stages after the ring fill (col_l2pf_d -1; 2/4/10/12 stages: 36.10/35.80/
-    # 36.01/36.46); issued NST stages earlier instead (col_l2pf_d >= 0) 39.5 us;
+    # 8 stages (2/4/10/12 stages: 36.10/35.80/36.01/36.46; the next tile's stages
+    # issued one ring depth before the current tile's end instead: 39.5 us, removed);
     # dycore (prologue kernels) +1 us, so off there
     l2pf = 0 if split else int((opts or {}).get("col_l2pf", 8 if sp.pro is None else 0))
-    l2pf_d = int((opts or {}).get("col_l2pf_d", -1))
     l2pf0 = int((opts or {}).get("col_l2pf0", 4 if sp.pro is None else 0))  # measured: vadv 256^2 38.22 -> 36.64 us; dycore neutral
     tm_params = ", ".join(f"const __grid_constant__ CUtensorMap tm_{f}" for f in tm_fields)
     if split:
@@ -629,7 +628,7 @@ def _emit_variant(kname, plan, sp: ThomasSpec, v: Variant, ctype, dtypes, opts):
         w(f"          gts_mbar_arrive_expect_tx(&full[s], {v.tx}u);")
         for f in tm_fields:
             w(f"          gts_tma_load_3d(smem + s * STB + {v.offs[f]}, &tm_{f}, &full[s], j0, i0, kb * {KB});")
-        if l2pf and l2pf_d < 0:
+        if l2pf:
             # default: once the ring holds this (non-first) tile's first NST
             # stages -- the previous tile's forward sweep is ending -- warm L2
             # with the next col_l2pf stages, streamed while its backward runs.
@@ -640,18 +639,6 @@ def _emit_variant(kname, plan, sp: ThomasSpec, v: Variant, ctype, dtypes, opts):
             w(f"            for (int q_ = NST; q_ < NST + {l2pf} && q_ < nkb; ++q_) {{")
             for f in tm_fields:
                 w(f"              gts_tma_prefetch_l2_3d(&tm_{f}, j0, i0, q_ * {KB});")
-            w("            }")
-            w("          }")
-        elif l2pf:
-            # warm L2 with the levels of this CTA's next tile that the ring
-            # will not hold when this tile's backward sweep starts, so HBM
-            # keeps streaming while the consumers run it
-            w(f"          if (kb == (nkb - 1 - {l2pf_d} > 0 ? nkb - 1 - {l2pf_d} : 0) && t + (int)gridDim.x < ntiles) {{")
-            w("            const int tn_ = t + (int)gridDim.x;")
-            w(f"            const int jn_ = (tn_ % tiles_j) * {TJ}, in_ = (tn_ / tiles_j) * {rows};")
-            w(f"            for (int q_ = NST; q_ < NST + {l2pf} && q_ < nkb; ++q_) {{")
-            for f in tm_fields:
-                w(f"              gts_tma_prefetch_l2_3d(&tm_{f}, jn_, in_, q_ * {KB});")
             w("            }")
             w("          }")
     w("        }")
