@@ -84,6 +84,10 @@ int gts_b200_abi_version(void);
 const char* gts_b200_error_string(int status);
 
 int gts_b200_device_count(int* count);
+/* NVTX ranges (header-only NVTX v3; no-ops without an attached tool): the
+ * backend wraps each call in "b200 <stencil>" when GTS_B200_NVTX=1. */
+int gts_b200_nvtx_push(const char* name);
+int gts_b200_nvtx_pop(void);
 int gts_b200_set_device(int device);
 int gts_b200_get_device(int* device);
 /* SM count, L2 bytes, compute capability (major*10+minor), HBM bytes. */

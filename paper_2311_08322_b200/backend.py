@@ -318,6 +318,8 @@ class device_timing:
 
 
 PIPE_TRACE = None  # a list to collect per-call device spans of the pipelined mirror mode (probes)
+# GTS_B200_NVTX=1: every call runs inside an NVTX range "b200 <stencil>" (nsys / ncu --nvtx filtering)
+NVTX = os.environ.get("GTS_B200_NVTX", "0") == "1"
 
 
 def _event(i: int):
@@ -675,4 +677,15 @@ def build(impl, fp, cache: Optional[BuildCache] = None, options: Optional[dict] 
         "plan": plan.describe(),
         "module": module,
     }
+    if NVTX:
+        label = f"b200 {impl.name}".encode()
+        inner = run
+
+        def run(domain, field_args, scalar_args) -> None:  # noqa: F811 - the NVTX-wrapped call
+            lib = native.lib()
+            lib.gts_b200_nvtx_push(label)
+            try:
+                inner(domain, field_args, scalar_args)
+            finally:
+                lib.gts_b200_nvtx_pop()
     return sf_common.ExecutableStencil(BACKEND_ID, fp, run, build_info)

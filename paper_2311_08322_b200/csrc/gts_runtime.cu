@@ -2,6 +2,7 @@
 // backend (declared in include/gts_b200.h).
 #include <cuda_profiler_api.h>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: no-ops unless a tool (nsys, ncu --nvtx) attaches
 #include <stdint.h>
 #include <stdio.h>
 #include <string.h>
@@ -30,6 +31,10 @@ GTS_EXPORT const char* gts_b200_error_string(int status) {
 }
 
 GTS_EXPORT int gts_b200_device_count(int* count) { return (int)cudaGetDeviceCount(count); }
+
+// NVTX ranges around backend calls (paper_2311_08322_b200.backend, GTS_B200_NVTX=1)
+GTS_EXPORT int gts_b200_nvtx_push(const char* name) { return nvtxRangePushA(name) < 0 ? 1 : 0; }
+GTS_EXPORT int gts_b200_nvtx_pop(void) { return nvtxRangePop() < 0 ? 1 : 0; }
 GTS_EXPORT int gts_b200_set_device(int device) { return (int)cudaSetDevice(device); }
 GTS_EXPORT int gts_b200_get_device(int* device) { return (int)cudaGetDevice(device); }
 

@@ -28,6 +28,8 @@ SIGNATURES = {
     "gts_b200_abi_version": (_INT, []),
     "gts_b200_error_string": (_c.c_char_p, [_INT]),
     "gts_b200_device_count": (_INT, [_c.POINTER(_INT)]),
+    "gts_b200_nvtx_push": (_INT, [_c.c_char_p]),
+    "gts_b200_nvtx_pop": (_INT, []),
     "gts_b200_set_device": (_INT, [_INT]),
     "gts_b200_get_device": (_INT, [_c.POINTER(_INT)]),
     "gts_b200_device_info": (_INT, [_INT, _c.POINTER(_INT), _c.POINTER(_INT), _c.POINTER(_INT),
