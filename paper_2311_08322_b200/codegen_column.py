@@ -546,8 +546,10 @@ def _emit_variant(kname, plan, sp: ThomasSpec, v: Variant, ctype, dtypes, opts):
     # Measured (tools/abtest.py, medians of 5): vadv 256^2 36.66 -> 35.56 us with
     # 8 stages (2/4/10/12 stages: 36.10/35.80/36.01/36.46; the next tile's stages
     # issued one ring depth before the current tile's end instead: 39.5 us, removed);
-    # dycore (prologue kernels) +1 us, so off there
-    l2pf = 0 if split else int((opts or {}).get("col_l2pf", 8 if sp.pro is None else 0))
+    # dycore (prologue kernels) +1 us, so off there.  With the two-CTA geometry
+    # (4-level stages) re-swept, medians of 7: 4/5/6/7/8 stages 35.02/34.94/34.91/
+    # 34.98/35.23 us
+    l2pf = 0 if split else int((opts or {}).get("col_l2pf", 6 if sp.pro is None else 0))
     l2pf0 = int((opts or {}).get("col_l2pf0", 4 if sp.pro is None else 0))  # measured: vadv 256^2 38.22 -> 36.64 us; dycore neutral
     tm_params = ", ".join(f"const __grid_constant__ CUtensorMap tm_{f}" for f in tm_fields)
     if split:
