@@ -550,7 +550,10 @@ def _emit_variant(kname, plan, sp: ThomasSpec, v: Variant, ctype, dtypes, opts):
     # (4-level stages) re-swept, medians of 7: 4/5/6/7/8 stages 35.02/34.94/34.91/
     # 34.98/35.23 us
     l2pf = 0 if split else int((opts or {}).get("col_l2pf", 6 if sp.pro is None else 0))
-    l2pf0 = int((opts or {}).get("col_l2pf0", 4 if sp.pro is None else 0))  # measured: vadv 256^2 38.22 -> 36.64 us; dycore neutral
+    # measured: vadv 256^2 38.22 -> 36.64 us with 4 stages (one-CTA geometry); dycore
+    # neutral; re-swept with the two-CTA geometry (medians of 7): 4/5/6/8 stages
+    # 34.89/34.77/34.79/34.97 us
+    l2pf0 = int((opts or {}).get("col_l2pf0", 5 if sp.pro is None else 0))
     tm_params = ", ".join(f"const __grid_constant__ CUtensorMap tm_{f}" for f in tm_fields)
     if split:
         tm_params += ", " + ", ".join(f"const __grid_constant__ CUtensorMap tm2_{f}" for f in tm_fields)
